@@ -1,0 +1,172 @@
+/*
+ * intscale_b200 — C ABI of the B200 (sm_100a) integer-scale W4A8 path.
+ *
+ * The reference (arXiv 2405.14597, /root/reference/proj) exposes its hot path
+ * as C++ free functions in namespace intscale (no FFI, no plugin registry). Each
+ * entry point below names the reference interface it replaces (file:line). The
+ * C++ drop-in layer (include/intscale/ headers) re-exposes the reference
+ * signatures on top of this ABI; the Python mirror binds it with ctypes.
+ *
+ * Conventions
+ *  - All tensor pointers are DEVICE pointers unless the name says _host.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls are stream-ordered and asynchronous unless documented otherwise,
+ *    reentrant, and never allocate device memory on the hot path (the GEMM
+ *    workspace is caller-owned; see isb_gemm_workspace_size).
+ *  - Return value: ISB_OK or an error code mapping 1:1 onto the reference
+ *    exception types (types.hpp:29-67); isb_last_error() gives the message
+ *    (thread-local).
+ *  - Data layouts are the reference's: activations row-major M x K, weights
+ *    row-major K x N (quantize.hpp:128-134, gemm.cpp:226), group scales with
+ *    unit = n * (K/g) + k/g (quantize.cpp:51), outputs row-major M x N.
+ */
+#ifndef INTSCALE_B200_H_
+#define INTSCALE_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum isb_status {
+  ISB_OK = 0,
+  ISB_PARAM = 1,     /* ParamError      types.hpp:55 */
+  ISB_DIMENSION = 2, /* DimensionError  types.hpp:50 */
+  ISB_VALUE = 3,     /* ValueError      types.hpp:44 */
+  ISB_OVERFLOW = 4,  /* OverflowError   types.hpp:61 */
+  ISB_LENGTH = 5,    /* LengthError     types.hpp:39 */
+  ISB_FORMAT = 6,    /* FormatError     types.hpp:34 */
+  ISB_ERROR = 7,     /* Error           types.hpp:29 */
+  ISB_CUDA = 8       /* CUDA runtime / launch failure (no reference analogue) */
+};
+
+enum isb_dtype { ISB_F32 = 0, ISB_BF16 = 1, ISB_F16 = 2 };
+
+enum isb_path { ISB_PATH_FLOAT_SCALE = 0, ISB_PATH_INTEGER_SCALE = 1 };
+
+const char* isb_last_error(void);
+int isb_version(void);
+/* Number of kernel launches this library has issued on the calling host
+ * thread's process since load (bench evidence; monotonic). */
+int64_t isb_launch_count(void);
+
+/* --------------------------------------------------------------------------
+ * K1 — per-token symmetric int8 activation quantizer.
+ * Replaces quantize(x, 8, Scheme::symmetric, Granularity::per_token())
+ * (quantize.hpp:146 / quantize.cpp:93-145). Bit-exact: codes are
+ * llround(double(x)/s) with s = max|x_row| / 127 (s = 1 for an all-zero row),
+ * never -128. Non-finite input => ISB_VALUE (checked: a device flag is read
+ * back, so this call synchronizes the stream when check_finite != 0).
+ */
+int isb_quantize_per_token(const void* x, int x_dtype, int64_t m, int64_t k, int8_t* codes,
+                           double* scales, int check_finite, void* stream);
+
+/* Group-wise symmetric weight quantizer, the offline step that feeds the
+ * packer: quantize(w, bits, symmetric, group_of(g)) (quantize.cpp:93-145,
+ * unit = n*(K/g) + k/g) for float32 K x N weights; codes written as int16
+ * (the reference MatQ container, types.hpp:21). per-channel == g = K. */
+int isb_quantize_weight_groups(const float* w, int64_t k, int64_t n, int64_t group,
+                               int bit_width, int16_t* codes, double* scales, void* stream);
+
+/* --------------------------------------------------------------------------
+ * K2 — offline int4 weight packer into the device layout.
+ * Source: reference int16 codes K x N (QuantizedTensor::values,
+ * quantize.hpp:128-130) or the reference packed_signed4 byte stream
+ * (tensor_io.hpp:62-66, tensor_io.cpp:179-193). Scales: the reference double
+ * group scales (n*(K/g)+k/g) and the IntegerScaleSet it was integerized into
+ * (integer_scale.hpp:17-21); int_scales may be NULL (float-scale only).
+ * Codes outside [-8, 7] => ISB_VALUE (pack_signed4 contract).
+ * The handle owns its device memory; destroy with isb_weight_destroy.
+ */
+typedef struct isb_weight isb_weight;
+
+int isb_weight_pack_codes(const int16_t* codes, int64_t k, int64_t n, int64_t group,
+                          const double* scales, const int32_t* int_scales, int64_t amplifier,
+                          void* stream, isb_weight** out);
+int isb_weight_pack_signed4(const uint8_t* bytes, int64_t nbytes, int64_t k, int64_t n,
+                            int64_t group, const double* scales, const int32_t* int_scales,
+                            int64_t amplifier, void* stream, isb_weight** out);
+/* Device verifier: writes the K x N int16 codes back (unpack_signed4,
+ * tensor_io.cpp:195-208, through the device layout). */
+int isb_weight_unpack_codes(const isb_weight* w, int16_t* codes, void* stream);
+/* Reference-order packed_signed4 bytes (ceil(K*N/2)) regenerated from the
+ * device layout; equals pack_signed4(codes) byte for byte. */
+int isb_weight_repack_signed4(const isb_weight* w, uint8_t* bytes, void* stream);
+int isb_weight_destroy(isb_weight* w);
+
+typedef struct {
+  int64_t k, n, group, groups, amplifier;
+  int32_t exponent;
+  int32_t has_int_scales;
+  int64_t packed_bytes;   /* HBM bytes of the int4 payload (padded to 128x128 tiles) */
+  int64_t scale_bytes;    /* HBM bytes of the per-tile int32 scales read by K3 */
+  int32_t max_int_scale;  /* max k_g (the k<=16 fold band) */
+  int32_t tensor_core_ok; /* 1 if group % 128 == 0 and K % 128 == 0 (K3/K4 eligible) */
+} isb_weight_info_t;
+int isb_weight_info(const isb_weight* w, isb_weight_info_t* info);
+
+/* --------------------------------------------------------------------------
+ * K3 / K4 — fused W4A8 GEMM on tcgen05 (kind::i8, TMEM accumulators).
+ * K3 replaces gemm_integer_scale (gemm.hpp:92, gemm.cpp:205-262):
+ *   out[i,j] = (double(sum_g P_g * k_g) / 2^e) * s_a[i], P_g int32 on the
+ *   tensor core, sum_g in int32 (exact when overflow_analyzer says safe).
+ * K4 replaces gemm_float_scale (gemm.hpp:82, gemm.cpp:156-203) in the
+ *   Atom-style fp32 form: acc += float(P_g) * float(s_g), one I2F + FFMA per
+ *   group and output.
+ * xq: int8 codes M x K; sa: double[M]. out: M x N in out_dtype.
+ * Requires K % 128 == 0 and group % 128 == 0 (isb_weight_info.tensor_core_ok);
+ * other shapes => ISB_PARAM (use isb_gemm_checked).
+ * The integer path does NOT check overflow: callers gate it with
+ * overflow_analyzer (analysis.cpp:24-59) as run_layer does (gemm.cpp:489-516).
+ * workspace: caller-owned device buffer of isb_gemm_workspace_size() bytes,
+ * zero-filled once before first use (the kernels leave it zeroed).
+ */
+int isb_gemm_workspace_size(int64_t m, const isb_weight* w, int64_t* bytes);
+int isb_gemm_integer_scale(const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                           const isb_weight* w, void* out, int out_dtype, void* workspace,
+                           int64_t workspace_bytes, void* stream);
+int isb_gemm_float_scale(const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                         const isb_weight* w, void* out, int out_dtype, void* workspace,
+                         int64_t workspace_bytes, void* stream);
+
+/* --------------------------------------------------------------------------
+ * Checked GEMM (CUDA cores, int64): the full reference semantics for any
+ * group size dividing K and for layers the static bound calls unsafe:
+ * per-group and running-accumulator 32-bit window tracking (gemm.cpp:42-52,
+ * :245-247), max_abs_accumulator, the lexicographically first overflowing
+ * output, the 2^62 hard limit, and NON-wrapped int64 results in permissive
+ * mode (gemm.cpp:90-98, :246-252). Float path: od += double(P_g)*s_g in
+ * double, bit-identical to gemm_float_scale.
+ * Optional outputs (NULL to skip): out f32, out_f64, acc (int64 M x N, integer
+ * path), partials (int64 signed P_g, M x (N*G), index (i, j*G+g)).
+ * Synchronous: stats are copied to the host before returning.
+ * strict != 0 and an overflow => ISB_OVERFLOW with the reference message
+ * "integer accumulation left the 32-bit window at output (i, j)".
+ */
+typedef struct {
+  int64_t max_abs_accumulator;
+  int32_t overflow_detected;
+  int32_t hard_limit_hit;
+  int64_t overflow_i, overflow_j;
+} isb_gemm_stats;
+
+int isb_gemm_checked(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                     const isb_weight* w, int strict, float* out, double* out_f64, int64_t* acc,
+                     int64_t* partials, isb_gemm_stats* stats, void* stream);
+
+/* Host-side helpers of the offline path (no device work). */
+/* overflow_analyzer (analysis.hpp:35, analysis.cpp:24-59). */
+int isb_overflow_analyzer(int64_t k, int64_t group, int act_bits, int weight_bits,
+                          const int32_t* int_scales_host, int64_t count, int64_t* static_bound,
+                          double* headroom_bits, int32_t* safe);
+/* search_amplifier_exponent / integerize_scales (integer_scale.cpp:21-59). */
+int isb_search_amplifier_exponent(const double* scales_host, int64_t count, int32_t* exponent);
+int isb_integerize_scales(const double* scales_host, int64_t count, int64_t amplifier,
+                          int32_t* int_scales_host, int32_t* exponent);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* INTSCALE_B200_H_ */

@@ -1,0 +1,431 @@
+// extern "C" boundary of libintscale_b200 (include/intscale_b200.h). Maps
+// failures onto the reference exception taxonomy (types.hpp:29-67) as status
+// codes; the C++ drop-in layer turns them back into exceptions.
+#include <atomic>
+#include <bit>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "layout.cuh"
+
+namespace isb {
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return ISB_OK;
+  } catch (const Failure& f) {
+    g_err = f.what();
+    return f.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return ISB_ERROR;
+  }
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int num_sms() {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  static std::mutex mu;
+  static std::vector<int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  if (static_cast<int>(cache.size()) <= dev) cache.resize(dev + 1, 0);
+  if (!cache[dev]) {
+    cuda_check(cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev),
+               "cudaDeviceGetAttribute");
+  }
+  return cache[dev];
+}
+
+// Per-device scratch int used as the "non-finite / bad code" flag when the
+// caller does not ask for the check (written, never read).
+int* scratch_flag() {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  static std::mutex mu;
+  static std::vector<int*> flags;
+  std::lock_guard<std::mutex> lk(mu);
+  if (static_cast<int>(flags.size()) <= dev) flags.resize(dev + 1, nullptr);
+  if (!flags[dev]) cuda_check(cudaMalloc(&flags[dev], 64), "cudaMalloc(flag)");
+  return flags[dev];
+}
+
+// Synchronous flag check for the offline / checked entry points.
+struct DeviceFlag {
+  int* d = nullptr;
+  explicit DeviceFlag(cudaStream_t s) {
+    cuda_check(cudaMalloc(&d, sizeof(int)), "cudaMalloc(flag)");
+    cuda_check(cudaMemsetAsync(d, 0, sizeof(int), s), "cudaMemsetAsync");
+  }
+  ~DeviceFlag() { cudaFree(d); }
+  bool raised(cudaStream_t s) {
+    int h = 0;
+    cuda_check(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s), "flag copy");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return h != 0;
+  }
+};
+
+int exponent_of(int64_t amp) {
+  if (amp < 1 || (amp & (amp - 1)) != 0)
+    fail(ISB_PARAM, "amplifier must be a power of two >= 1, got " + std::to_string(amp));
+  return std::countr_zero(static_cast<uint64_t>(amp));
+}
+
+void require_positive_scales(const double* s, int64_t n) {  // integer_scale.cpp:13-18
+  if (n == 0) fail(ISB_PARAM, "scale list is empty");
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(s[i]) || s[i] <= 0.0)
+      fail(ISB_PARAM, "scale " + std::to_string(i) + " is not a positive finite number");
+}
+
+isb_weight* pack_common(const int16_t* codes, const uint8_t* s4, int64_t k, int64_t n,
+                        int64_t group, const double* scales, const int32_t* int_scales,
+                        int64_t amplifier, cudaStream_t s) {
+  if (k < 1 || n < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+  if (group < 1) fail(ISB_PARAM, "group size must be >= 1");
+  if (k % group != 0)
+    fail(ISB_PARAM, "group size " + std::to_string(group) +
+                        " does not divide the reduction dimension " + std::to_string(k));
+  if (!scales) fail(ISB_PARAM, "weight scales are required");
+  auto* w = new isb_weight();
+  try {
+    w->k = k;
+    w->n = n;
+    w->group = group;
+    w->groups = k / group;
+    w->amplifier = int_scales ? amplifier : 1;
+    w->exponent = int_scales ? exponent_of(amplifier) : 0;
+    w->has_int_scales = int_scales != nullptr;
+    w->kblocks = (k + kBlockK - 1) / kBlockK;
+    w->n_tiles = (n + kTileN - 1) / kTileN;
+    w->packed_bytes = w->n_tiles * w->kblocks * kBlockBytes;
+    const int64_t units = n * w->groups;
+    cuda_check(cudaMalloc(&w->packed, w->packed_bytes), "cudaMalloc(packed)");
+    cuda_check(cudaMalloc(&w->scales, units * sizeof(double)), "cudaMalloc(scales)");
+    cuda_check(cudaMemcpyAsync(w->scales, scales, units * sizeof(double), cudaMemcpyDefault, s),
+               "copy scales");
+    if (int_scales) {
+      cuda_check(cudaMalloc(&w->int_scales, units * sizeof(int32_t)), "cudaMalloc(int_scales)");
+      cuda_check(cudaMemcpyAsync(w->int_scales, int_scales, units * sizeof(int32_t),
+                                 cudaMemcpyDefault, s),
+                 "copy int scales");
+      std::vector<int32_t> h(static_cast<size_t>(units));
+      cuda_check(cudaMemcpyAsync(h.data(), int_scales, units * sizeof(int32_t), cudaMemcpyDefault,
+                                 s),
+                 "copy int scales to host");
+      cuda_check(cudaStreamSynchronize(s), "sync");
+      int32_t mx = 0;
+      for (int32_t v : h) {
+        if (v < 1) fail(ISB_PARAM, "integer scales must be >= 1");
+        mx = std::max(mx, v);
+      }
+      w->max_int_scale = mx;
+    }
+    DeviceFlag bad(s);
+    launch_pack(codes, s4, k, n, w->packed, w->kblocks, w->n_tiles, bad.d, s);
+    if (w->tensor_core_ok()) {
+      const int64_t tiled = w->n_tiles * w->groups * kTileN;
+      cuda_check(cudaMalloc(&w->fscale_tiled, tiled * sizeof(float)), "cudaMalloc(fscale)");
+      if (int_scales)
+        cuda_check(cudaMalloc(&w->kscale_tiled, tiled * sizeof(int32_t)), "cudaMalloc(kscale)");
+      launch_tile_scales(w->int_scales, w->scales, n, w->groups, w->n_tiles, w->kscale_tiled,
+                         w->fscale_tiled, s);
+    }
+    if (bad.raised(s)) {
+      if (codes) fail(ISB_VALUE, "weight codes outside signed 4-bit range [-8, 7]");
+      fail(ISB_VALUE, "packed payload decodes outside [-8, 7]");
+    }
+  } catch (...) {
+    isb_weight_destroy(w);
+    throw;
+  }
+  return w;
+}
+
+void require_gemm_args(const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                       const isb_weight* w, int out_dtype) {
+  if (!w) fail(ISB_PARAM, "null weight handle");
+  if (!xq || !sa) fail(ISB_PARAM, "null activation pointer");
+  if (m < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+  if (k != w->k)
+    fail(ISB_DIMENSION,
+         "activation K=" + std::to_string(k) + " vs weight rows " + std::to_string(w->k));
+  if (out_dtype != ISB_F32 && out_dtype != ISB_BF16 && out_dtype != ISB_F16)
+    fail(ISB_PARAM, "unsupported output dtype");
+}
+
+void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
+             const isb_weight* w, void* out, int out_dtype, void* ws, int64_t ws_bytes,
+             void* stream) {
+  require_gemm_args(xq, sa, m, k, w, out_dtype);
+  if (!w->tensor_core_ok())
+    fail(ISB_PARAM, "tcgen05 path needs K % 128 == 0 and group % 128 == 0 (use isb_gemm_checked)");
+  if (path == ISB_PATH_INTEGER_SCALE && !w->has_int_scales)
+    fail(ISB_PARAM, "integer-scale path needs an IntegerScaleSet");
+  if (m > std::numeric_limits<int>::max() || w->n > std::numeric_limits<int>::max())
+    fail(ISB_PARAM, "shape too large");
+  const GemmPlan pl = plan_gemm(m, *w, num_sms());
+  if (!ws || ws_bytes < pl.workspace_bytes)
+    fail(ISB_PARAM, "workspace too small: need " + std::to_string(pl.workspace_bytes) + " bytes");
+  launch_gemm_tc(path, xq, sa, m, *w, out, out_dtype, ws, pl, as_stream(stream));
+}
+
+}  // namespace
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+}  // namespace isb
+
+using namespace isb;
+
+extern "C" {
+
+const char* isb_last_error(void) { return g_err.c_str(); }
+int isb_version(void) { return 1; }
+int64_t isb_launch_count(void) { return g_launches.load(); }
+
+int isb_quantize_per_token(const void* x, int x_dtype, int64_t m, int64_t k, int8_t* codes,
+                           double* scales, int check_finite, void* stream) {
+  return guarded([&] {
+    if (m < 1 || k < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+    if (!x || !codes || !scales) fail(ISB_PARAM, "null pointer");
+    cudaStream_t s = as_stream(stream);
+    if (check_finite) {
+      DeviceFlag bad(s);
+      launch_quantize_per_token(x, x_dtype, m, k, codes, scales, bad.d, s);
+      if (bad.raised(s)) fail(ISB_VALUE, "input has non-finite values");
+    } else {
+      launch_quantize_per_token(x, x_dtype, m, k, codes, scales, scratch_flag(), s);
+    }
+  });
+}
+
+int isb_quantize_weight_groups(const float* w, int64_t k, int64_t n, int64_t group,
+                               int bit_width, int16_t* codes, double* scales, void* stream) {
+  return guarded([&] {
+    if (bit_width != 4 && bit_width != 8)
+      fail(ISB_PARAM, "bit width must be 4 or 8, got " + std::to_string(bit_width));
+    if (k < 1 || n < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+    if (group < 1) fail(ISB_PARAM, "group size must be >= 1");
+    if (k % group != 0)
+      fail(ISB_PARAM, "group size " + std::to_string(group) +
+                          " does not divide the reduction dimension " + std::to_string(k));
+    cudaStream_t s = as_stream(stream);
+    DeviceFlag bad(s);
+    launch_quantize_weight_groups(w, k, n, group, bit_width, codes, scales, bad.d, s);
+    if (bad.raised(s)) fail(ISB_VALUE, "input has non-finite values");
+  });
+}
+
+int isb_weight_pack_codes(const int16_t* codes, int64_t k, int64_t n, int64_t group,
+                          const double* scales, const int32_t* int_scales, int64_t amplifier,
+                          void* stream, isb_weight** out) {
+  return guarded([&] {
+    if (!codes || !out) fail(ISB_PARAM, "null pointer");
+    *out = pack_common(codes, nullptr, k, n, group, scales, int_scales, amplifier,
+                       as_stream(stream));
+  });
+}
+
+int isb_weight_pack_signed4(const uint8_t* bytes, int64_t nbytes, int64_t k, int64_t n,
+                            int64_t group, const double* scales, const int32_t* int_scales,
+                            int64_t amplifier, void* stream, isb_weight** out) {
+  return guarded([&] {
+    if (!bytes || !out) fail(ISB_PARAM, "null pointer");
+    if (nbytes != (k * n + 1) / 2)  // unpack_signed4 contract, tensor_io.cpp:197-199
+      fail(ISB_LENGTH, "packed payload is " + std::to_string(nbytes) + " bytes, expected " +
+                           std::to_string((k * n + 1) / 2));
+    *out = pack_common(nullptr, bytes, k, n, group, scales, int_scales, amplifier,
+                       as_stream(stream));
+  });
+}
+
+int isb_weight_unpack_codes(const isb_weight* w, int16_t* codes, void* stream) {
+  return guarded([&] {
+    if (!w || !codes) fail(ISB_PARAM, "null pointer");
+    launch_unpack(*w, codes, as_stream(stream));
+  });
+}
+
+int isb_weight_repack_signed4(const isb_weight* w, uint8_t* bytes, void* stream) {
+  return guarded([&] {
+    if (!w || !bytes) fail(ISB_PARAM, "null pointer");
+    launch_repack_signed4(*w, bytes, as_stream(stream));
+  });
+}
+
+int isb_weight_destroy(isb_weight* w) {
+  if (!w) return ISB_OK;
+  cudaFree(w->packed);
+  cudaFree(w->kscale_tiled);
+  cudaFree(w->fscale_tiled);
+  cudaFree(w->int_scales);
+  cudaFree(w->scales);
+  delete w;
+  return ISB_OK;
+}
+
+int isb_weight_info(const isb_weight* w, isb_weight_info_t* info) {
+  return guarded([&] {
+    if (!w || !info) fail(ISB_PARAM, "null pointer");
+    info->k = w->k;
+    info->n = w->n;
+    info->group = w->group;
+    info->groups = w->groups;
+    info->amplifier = w->amplifier;
+    info->exponent = w->exponent;
+    info->has_int_scales = w->has_int_scales;
+    info->packed_bytes = w->packed_bytes;
+    info->scale_bytes = w->tensor_core_ok() ? w->n_tiles * w->groups * kTileN * 4 : 0;
+    info->max_int_scale = w->max_int_scale;
+    info->tensor_core_ok = w->tensor_core_ok() ? 1 : 0;
+  });
+}
+
+int isb_gemm_workspace_size(int64_t m, const isb_weight* w, int64_t* bytes) {
+  return guarded([&] {
+    if (!w || !bytes) fail(ISB_PARAM, "null pointer");
+    if (m < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+    *bytes = w->tensor_core_ok() ? plan_gemm(m, *w, num_sms()).workspace_bytes : 0;
+  });
+}
+
+int isb_gemm_integer_scale(const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                           const isb_weight* w, void* out, int out_dtype, void* workspace,
+                           int64_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    gemm_tc(ISB_PATH_INTEGER_SCALE, xq, sa, m, k, w, out, out_dtype, workspace, workspace_bytes,
+            stream);
+  });
+}
+
+int isb_gemm_float_scale(const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                         const isb_weight* w, void* out, int out_dtype, void* workspace,
+                         int64_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    gemm_tc(ISB_PATH_FLOAT_SCALE, xq, sa, m, k, w, out, out_dtype, workspace, workspace_bytes,
+            stream);
+  });
+}
+
+int isb_gemm_checked(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                     const isb_weight* w, int strict, float* out, double* out_f64, int64_t* acc,
+                     int64_t* partials, isb_gemm_stats* stats, void* stream) {
+  return guarded([&] {
+    require_gemm_args(xq, sa, m, k, w, ISB_F32);
+    if (path == ISB_PATH_INTEGER_SCALE && !w->has_int_scales)
+      fail(ISB_PARAM, "integer-scale path needs an IntegerScaleSet");
+    cudaStream_t s = as_stream(stream);
+    unsigned long long* d = nullptr;
+    cuda_check(cudaMalloc(&d, 3 * sizeof(unsigned long long)), "cudaMalloc(stats)");
+    unsigned long long h[3] = {0ull, ~0ull, ~0ull};
+    try {
+      cuda_check(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, s), "stats init");
+      launch_gemm_checked(path, xq, sa, m, *w, out, out_f64, acc, partials, d, s);
+      cuda_check(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s), "stats copy");
+      cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    } catch (...) {
+      cudaFree(d);
+      throw;
+    }
+    cudaFree(d);
+    const int64_t n = w->n;
+    isb_gemm_stats st{};
+    st.max_abs_accumulator = static_cast<int64_t>(h[0]);
+    st.overflow_detected = h[1] != ~0ull;
+    st.hard_limit_hit = h[2] != ~0ull;
+    st.overflow_i = st.overflow_detected ? static_cast<int64_t>(h[1]) / n : -1;
+    st.overflow_j = st.overflow_detected ? static_cast<int64_t>(h[1]) % n : -1;
+    if (stats) *stats = st;
+    if (st.hard_limit_hit)  // gemm.cpp:49-51
+      fail(ISB_ERROR, "accumulator exceeded the 64-bit safety margin at output (" +
+                          std::to_string(static_cast<int64_t>(h[2]) / n) + ", " +
+                          std::to_string(static_cast<int64_t>(h[2]) % n) + ")");
+    if (st.overflow_detected && strict)  // gemm.cpp:96-98
+      fail(ISB_OVERFLOW, "integer accumulation left the 32-bit window at output (" +
+                             std::to_string(st.overflow_i) + ", " + std::to_string(st.overflow_j) +
+                             ")");
+  });
+}
+
+int isb_overflow_analyzer(int64_t k, int64_t group, int act_bits, int weight_bits,
+                          const int32_t* int_scales, int64_t count, int64_t* static_bound,
+                          double* headroom_bits, int32_t* safe) {
+  // analysis.cpp:24-59
+  return guarded([&] {
+    if (act_bits != 4 && act_bits != 8) fail(ISB_PARAM, "activation bits must be 4 or 8");
+    if (weight_bits != 4 && weight_bits != 8) fail(ISB_PARAM, "weight bits must be 4 or 8");
+    if (k < 1 || group < 1 || k % group != 0) fail(ISB_PARAM, "group size must divide K");
+    const int64_t groups = k / group;
+    if (count < groups || count % groups != 0)
+      fail(ISB_PARAM, "integer scale count incompatible with the grouping");
+    for (int64_t i = 0; i < count; ++i)
+      if (int_scales[i] < 1) fail(ISB_PARAM, "integer scales must be >= 1");
+    const int64_t a_max = (int64_t{1} << (act_bits - 1)) - 1;
+    const int64_t w_max = int64_t{1} << (weight_bits - 1);
+    const auto per_mac = static_cast<unsigned __int128>(group) * a_max * w_max;
+    unsigned __int128 worst = 0;
+    for (int64_t c = 0; c < count / groups; ++c) {
+      unsigned __int128 col = 0;
+      for (int64_t g = 0; g < groups; ++g)
+        col += per_mac * static_cast<unsigned __int128>(int_scales[c * groups + g]);
+      worst = std::max(worst, col);
+    }
+    const auto cap = static_cast<unsigned __int128>(std::numeric_limits<int64_t>::max());
+    const int64_t bound = worst > cap ? std::numeric_limits<int64_t>::max()
+                                      : static_cast<int64_t>(worst);
+    const int64_t hi = std::numeric_limits<int32_t>::max();
+    if (static_bound) *static_bound = bound;
+    if (safe) *safe = bound <= hi;
+    if (headroom_bits)
+      *headroom_bits = std::log2(static_cast<double>(hi)) - std::log2(static_cast<double>(bound));
+  });
+}
+
+int isb_search_amplifier_exponent(const double* scales, int64_t count, int32_t* exponent) {
+  // integer_scale.cpp:21-34: double min(s) until >= 1 (exact doublings).
+  return guarded([&] {
+    require_positive_scales(scales, count);
+    double a = scales[0];
+    for (int64_t i = 1; i < count; ++i) a = std::min(a, scales[i]);
+    int e = 0;
+    while (a < 1.0) {
+      if (e >= 62) fail(ISB_PARAM, "smallest scale is too small to amplify");
+      a *= 2.0;
+      ++e;
+    }
+    *exponent = e;
+  });
+}
+
+int isb_integerize_scales(const double* scales, int64_t count, int64_t amplifier,
+                          int32_t* int_scales, int32_t* exponent) {
+  // integer_scale.cpp:40-59: k = max(1, llround(s * amp)), OverflowError past int32.
+  return guarded([&] {
+    require_positive_scales(scales, count);
+    const int e = exponent_of(amplifier);
+    for (int64_t i = 0; i < count; ++i) {
+      const int64_t kk = std::llround(scales[i] * static_cast<double>(amplifier));
+      if (kk > std::numeric_limits<int32_t>::max())
+        fail(ISB_OVERFLOW, "amplified scale " + std::to_string(i) +
+                               " exceeds int32; amplifier too large for this scale set");
+      int_scales[i] = static_cast<int32_t>(std::max<int64_t>(kk, 1));
+    }
+    *exponent = e;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// Internal declarations shared by the translation units of libintscale_b200.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/intscale_b200.h"
+
+struct isb_weight {
+  int64_t k = 0, n = 0, group = 0, groups = 0, amplifier = 1;
+  int32_t exponent = 0;
+  int32_t has_int_scales = 0;
+  int32_t max_int_scale = 0;
+  int64_t kblocks = 0;   // ceil(K / 128)
+  int64_t n_tiles = 0;   // ceil(N / 128)
+  uint8_t* packed = nullptr;        // n_tiles * kblocks * 8 KiB
+  int32_t* kscale_tiled = nullptr;  // [n_tiles][groups][128] int32 (group % 128 == 0 only)
+  float* fscale_tiled = nullptr;    // [n_tiles][groups][128] float(s) / 16
+  int32_t* int_scales = nullptr;    // raw [N * groups] (reference unit order)
+  double* scales = nullptr;         // raw [N * groups]
+  int64_t packed_bytes = 0;
+  bool tensor_core_ok() const { return group % 128 == 0 && k % 128 == 0; }
+};
+
+namespace isb {
+
+struct Failure : std::runtime_error {
+  int code;
+  Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Failure(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(ISB_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void count_launch(int n = 1);
+
+// Kernel launchers (defined in the .cu files).
+void launch_quantize_per_token(const void* x, int x_dtype, int64_t m, int64_t k, int8_t* codes,
+                               double* scales, int* bad_flag, cudaStream_t s);
+void launch_quantize_weight_groups(const float* w, int64_t k, int64_t n, int64_t group, int bits,
+                                   int16_t* codes, double* scales, int* bad_flag, cudaStream_t s);
+void launch_pack(const int16_t* codes, const uint8_t* signed4, int64_t k, int64_t n,
+                 uint8_t* packed, int64_t kblocks, int64_t n_tiles, int* bad_flag, cudaStream_t s);
+void launch_tile_scales(const int32_t* int_scales, const double* scales, int64_t n,
+                        int64_t groups, int64_t n_tiles, int32_t* kscale, float* fscale,
+                        cudaStream_t s);
+void launch_unpack(const isb_weight& w, int16_t* codes, cudaStream_t s);
+void launch_repack_signed4(const isb_weight& w, uint8_t* bytes, cudaStream_t s);
+
+struct GemmPlan {
+  int mt = 0;         // tokens per tile (UMMA N)
+  int m_tiles = 0;
+  int tiles = 0;
+  int64_t units = 0;  // tiles * groups
+  int grid = 0;
+  int maxc = 1;       // max CTAs contributing to one tile
+  int64_t workspace_bytes = 0;
+};
+GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms);
+void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
+                    void* out, int out_dtype, void* workspace, const GemmPlan& plan,
+                    cudaStream_t s);
+void launch_gemm_checked(int path, const int8_t* xq, const double* sa, int64_t m,
+                         const isb_weight& w, float* out, double* out_f64, int64_t* acc,
+                         int64_t* partials, unsigned long long* stats_dev, cudaStream_t s);
+
+}  // namespace isb

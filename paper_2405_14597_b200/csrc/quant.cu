@@ -1,0 +1,221 @@
+// K1 — per-token symmetric int8 activation quantizer, and the offline group
+// weight quantizer that feeds the packer.
+//
+// Reference semantics: quantize(x, 8, symmetric, per_token) and
+// quantize(w, 4, symmetric, group_of(g)), quantize.cpp:93-145:
+//   s = max(|min|, |max|) / qmax over the unit (s = 1 when the unit is all 0),
+//   q = clamp(llround(double(x) / s), qmin, qmax)   (round half away from zero)
+// Both are reproduced bit-exactly.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace isb {
+namespace {
+
+constexpr int kQuantThreads = 256;
+
+// llround(double(x) / s) with the division replaced by a multiply by the
+// reciprocal except within 1e-9 of a rounding tie, where the exact IEEE
+// quotient decides. |y - x/s| <= ~4e-14 for |x/s| <= 127, so outside that
+// window round(y) == llround(RN(x/s)).
+__device__ __forceinline__ int quant_one(float xf, double s, double r, int qmin, int qmax) {
+  const double x = static_cast<double>(xf);
+  const double y = x * r;
+  const double ay = fabs(y);
+  const double frac = ay - floor(ay);
+  double q = (fabs(frac - 0.5) > 1e-9) ? round(y) : round(x / s);
+  q = fmin(fmax(q, static_cast<double>(qmin)), static_cast<double>(qmax));
+  return static_cast<int>(q);
+}
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < kQuantThreads / 32 ? red[l] : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (l == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float r = red[0];
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ void load4(const T* p, float (&v)[4]);
+
+template <>
+__device__ __forceinline__ void load4<float>(const float* p, float (&v)[4]) {
+  const float4 f = __ldg(reinterpret_cast<const float4*>(p));
+  v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+}
+
+template <>
+__device__ __forceinline__ void load4<__nv_bfloat16>(const __nv_bfloat16* p, float (&v)[4]) {
+  const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+  v[0] = __uint_as_float(u.x << 16);
+  v[1] = __uint_as_float(u.x & 0xFFFF0000u);
+  v[2] = __uint_as_float(u.y << 16);
+  v[3] = __uint_as_float(u.y & 0xFFFF0000u);
+}
+
+template <typename T>
+__device__ __forceinline__ float load1(const T* p);
+template <>
+__device__ __forceinline__ float load1<float>(const float* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ float load1<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat162float(*p);
+}
+
+// One CTA per token row; the row stays in registers (V x 4 elements per
+// thread), so HBM is read exactly once: M*K*sizeof(T) in, M*K + 8M out.
+template <int V, typename T>
+__global__ void __launch_bounds__(kQuantThreads)
+    quantize_rows_cached(const T* __restrict__ x, int64_t k, int8_t* __restrict__ codes,
+                         double* __restrict__ scales, int* __restrict__ bad) {
+  __shared__ float red[kQuantThreads / 32];
+  const int64_t row = blockIdx.x;
+  const T* xr = x + row * k;
+  float v[V][4];
+  float amax = 0.0f;
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int64_t e = (static_cast<int64_t>(i) * kQuantThreads + threadIdx.x) * 4;
+    if (e < k) {
+      load4<T>(xr + e, v[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        finite = finite && isfinite(v[i][j]);
+        amax = fmaxf(amax, fabsf(v[i][j]));
+      }
+    }
+  }
+  if (!finite) atomicExch(bad, 1);
+  amax = block_max(amax, red);
+  const double s = amax == 0.0f ? 1.0 : static_cast<double>(amax) / 127.0;
+  const double r = 1.0 / s;
+  if (threadIdx.x == 0) scales[row] = s;
+  int8_t* cr = codes + row * k;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int64_t e = (static_cast<int64_t>(i) * kQuantThreads + threadIdx.x) * 4;
+    if (e < k) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        packed |= (static_cast<uint32_t>(quant_one(v[i][j], s, r, -128, 127)) & 0xFFu) << (8 * j);
+      *reinterpret_cast<uint32_t*>(cr + e) = packed;
+    }
+  }
+}
+
+// Any K / alignment: two passes over the row (the second hits L2).
+template <typename T>
+__global__ void __launch_bounds__(kQuantThreads)
+    quantize_rows_generic(const T* __restrict__ x, int64_t k, int8_t* __restrict__ codes,
+                          double* __restrict__ scales, int* __restrict__ bad) {
+  __shared__ float red[kQuantThreads / 32];
+  const int64_t row = blockIdx.x;
+  const T* xr = x + row * k;
+  float amax = 0.0f;
+  bool finite = true;
+  for (int64_t e = threadIdx.x; e < k; e += kQuantThreads) {
+    const float f = load1<T>(xr + e);
+    finite = finite && isfinite(f);
+    amax = fmaxf(amax, fabsf(f));
+  }
+  if (!finite) atomicExch(bad, 1);
+  amax = block_max(amax, red);
+  const double s = amax == 0.0f ? 1.0 : static_cast<double>(amax) / 127.0;
+  const double r = 1.0 / s;
+  if (threadIdx.x == 0) scales[row] = s;
+  for (int64_t e = threadIdx.x; e < k; e += kQuantThreads)
+    codes[row * k + e] = static_cast<int8_t>(quant_one(load1<T>(xr + e), s, r, -128, 127));
+}
+
+// Offline group quantizer: one thread per (column n, group t); consecutive
+// threads take consecutive columns so every row read is coalesced.
+__global__ void quantize_weight_groups_kernel(const float* __restrict__ w, int64_t k, int64_t n,
+                                              int64_t g, int bits, int16_t* __restrict__ codes,
+                                              double* __restrict__ scales, int* __restrict__ bad) {
+  const int64_t groups = k / g;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= n * groups) return;
+  const int64_t c = idx % n, t = idx / n;
+  const int qmax = (1 << (bits - 1)) - 1, qmin = -(1 << (bits - 1));
+  double amax = 0.0;
+  bool finite = true;
+  for (int64_t r = t * g; r < (t + 1) * g; ++r) {
+    const float v = w[r * n + c];
+    finite = finite && isfinite(v);
+    amax = fmax(amax, fabs(static_cast<double>(v)));
+  }
+  if (!finite) atomicExch(bad, 1);
+  const double s = amax == 0.0 ? 1.0 : amax / static_cast<double>(qmax);
+  scales[c * groups + t] = s;  // unit = c * (K/g) + r/g   (quantize.cpp:51)
+  for (int64_t r = t * g; r < (t + 1) * g; ++r) {
+    double q = round(static_cast<double>(w[r * n + c]) / s);
+    q = fmin(fmax(q, static_cast<double>(qmin)), static_cast<double>(qmax));
+    codes[r * n + c] = static_cast<int16_t>(q);
+  }
+}
+
+template <typename T>
+void launch_rows(const T* x, int64_t m, int64_t k, int8_t* codes, double* scales, int* bad,
+                 cudaStream_t s) {
+  const bool vec_ok = (k % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % (4 * sizeof(T)) == 0) &&
+                      (reinterpret_cast<uintptr_t>(codes) % 4 == 0);
+  const int64_t per_pass = static_cast<int64_t>(kQuantThreads) * 4;
+  const int64_t v = (k + per_pass - 1) / per_pass;
+  const dim3 grid(static_cast<unsigned>(m));
+  if (vec_ok && v <= 1) {
+    quantize_rows_cached<1, T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
+  } else if (vec_ok && v <= 2) {
+    quantize_rows_cached<2, T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
+  } else if (vec_ok && v <= 4) {
+    quantize_rows_cached<4, T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
+  } else if (vec_ok && v <= 8) {
+    quantize_rows_cached<8, T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
+  } else if (vec_ok && v <= 14) {
+    quantize_rows_cached<14, T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
+  } else {
+    quantize_rows_generic<T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
+  }
+  cuda_check(cudaGetLastError(), "quantize_per_token launch");
+  count_launch();
+}
+
+}  // namespace
+
+void launch_quantize_per_token(const void* x, int x_dtype, int64_t m, int64_t k, int8_t* codes,
+                               double* scales, int* bad, cudaStream_t s) {
+  if (x_dtype == ISB_F32)
+    launch_rows(static_cast<const float*>(x), m, k, codes, scales, bad, s);
+  else if (x_dtype == ISB_BF16)
+    launch_rows(static_cast<const __nv_bfloat16*>(x), m, k, codes, scales, bad, s);
+  else
+    fail(ISB_PARAM, "activation dtype must be float32 or bfloat16");
+}
+
+void launch_quantize_weight_groups(const float* w, int64_t k, int64_t n, int64_t group,
+                                        int bits, int16_t* codes, double* scales, int* bad,
+                                        cudaStream_t s) {
+  const int64_t total = n * (k / group);
+  const int threads = 256;
+  const int64_t blocks = (total + threads - 1) / threads;
+  quantize_weight_groups_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(
+      w, k, n, group, bits, codes, scales, bad);
+  cuda_check(cudaGetLastError(), "quantize_weight_groups launch");
+  count_launch();
+}
+
+}  // namespace isb

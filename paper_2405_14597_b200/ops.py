@@ -1,0 +1,273 @@
+"""Python host mirror of the reference operator API for the hot path, over the
+C ABI (include/intscale_b200.h). Names and argument meaning follow the
+reference (proj/include/intscale/*.hpp); tensors are torch CUDA tensors used
+purely as device memory. Every compute call runs a CUDA kernel of
+libintscale_b200.so — nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (ISB_BF16, ISB_F16, ISB_F32, ISB_PATH_FLOAT_SCALE, ISB_PATH_INTEGER_SCALE,
+                   GemmStats, WeightInfo, check, load)
+
+_DT = {torch.float32: ISB_F32, torch.bfloat16: ISB_BF16, torch.float16: ISB_F16}
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _cuda(t, dtype=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise _lib.ParamError("expected a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise _lib.ParamError(f"expected dtype {dtype}, got {t.dtype}")
+    return t.contiguous()
+
+
+# ---------------------------------------------------------------------------- K1
+def quantize_per_token(x: torch.Tensor, check_finite: bool = False, stream=None):
+    """quantize(x, 8, symmetric, per_token) — quantize.cpp:93-145. Returns
+    (codes int8 [M, K], scales float64 [M])."""
+    x = _cuda(x)
+    if x.dtype not in (torch.float32, torch.bfloat16):
+        raise _lib.ParamError("activations must be float32 or bfloat16")
+    if x.dim() != 2:
+        raise _lib.ParamError("activations must be 2-d")
+    m, k = x.shape
+    codes = torch.empty((m, k), dtype=torch.int8, device=x.device)
+    scales = torch.empty((m,), dtype=torch.float64, device=x.device)
+    check(load().isb_quantize_per_token(_ptr(x), _DT[x.dtype], m, k, _ptr(codes), _ptr(scales),
+                                        int(check_finite), _stream(stream)))
+    return codes, scales
+
+
+def quantize_weight(w: torch.Tensor, group: int = 128, bit_width: int = 4, stream=None):
+    """quantize(w, bits, symmetric, group_of(g)) — quantize.cpp:93-145. Returns
+    (codes int16 [K, N], scales float64 [N * K/g], unit n*(K/g)+k/g)."""
+    w = _cuda(w, torch.float32)
+    k, n = w.shape
+    codes = torch.empty((k, n), dtype=torch.int16, device=w.device)
+    scales = torch.empty((n * (k // group) if group > 0 and k % group == 0 else 1,),
+                         dtype=torch.float64, device=w.device)
+    check(load().isb_quantize_weight_groups(_ptr(w), k, n, group, bit_width, _ptr(codes),
+                                            _ptr(scales), _stream(stream)))
+    return codes, scales
+
+
+# ---------------------------------------------------------------------------- host helpers
+@dataclass
+class IntegerScaleSet:
+    """integer_scale.hpp:17-21."""
+    int_scales: np.ndarray
+    amplifier: int
+    exponent: int
+
+
+def search_amplifier_exponent(scales) -> int:
+    s = np.ascontiguousarray(np.asarray(scales, np.float64))
+    e = C.c_int32()
+    check(load().isb_search_amplifier_exponent(s.ctypes.data_as(C.c_void_p), s.size, C.byref(e)))
+    return e.value
+
+
+def search_amplifier(scales) -> int:
+    return 1 << search_amplifier_exponent(scales)
+
+
+def integerize_scales(scales, amplifier: int) -> IntegerScaleSet:
+    s = np.ascontiguousarray(np.asarray(scales, np.float64))
+    out = np.empty(max(s.size, 1), np.int32)
+    e = C.c_int32()
+    check(load().isb_integerize_scales(s.ctypes.data_as(C.c_void_p), s.size, int(amplifier),
+                                       out.ctypes.data_as(C.c_void_p), C.byref(e)))
+    return IntegerScaleSet(out[: s.size], int(amplifier), e.value)
+
+
+def overflow_analyzer(k: int, group: int, act_bits: int, weight_bits: int, s: IntegerScaleSet):
+    ks = np.ascontiguousarray(np.asarray(s.int_scales, np.int32))
+    bound, head, safe = C.c_int64(), C.c_double(), C.c_int32()
+    check(load().isb_overflow_analyzer(k, group, act_bits, weight_bits,
+                                       ks.ctypes.data_as(C.c_void_p), ks.size, C.byref(bound),
+                                       C.byref(head), C.byref(safe)))
+    return {"static_bound": bound.value, "observed_max": 0, "headroom_bits": head.value,
+            "safe": bool(safe.value)}
+
+
+# ---------------------------------------------------------------------------- K2
+class PackedWeight:
+    """Device-resident int4 weight in the tiled layout (csrc/layout.cuh) plus its
+    group scales and IntegerScaleSet. Owns the C handle."""
+
+    def __init__(self, handle: C.c_void_p, device):
+        self._h = handle
+        self.device = device
+        info = WeightInfo()
+        check(load().isb_weight_info(self._h, C.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in WeightInfo._fields_}
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def k(self):
+        return self.info["k"]
+
+    @property
+    def n(self):
+        return self.info["n"]
+
+    @property
+    def group(self):
+        return self.info["group"]
+
+    @staticmethod
+    def _scales(scales, int_scales, device):
+        s = torch.as_tensor(scales, dtype=torch.float64).to(device).contiguous()
+        ks = None
+        if int_scales is not None:
+            ks = torch.as_tensor(np.asarray(int_scales, np.int32) if not isinstance(
+                int_scales, torch.Tensor) else int_scales, dtype=torch.int32).to(device).contiguous()
+        return s, ks
+
+    @classmethod
+    def from_codes(cls, codes: torch.Tensor, group: int, scales, int_scales=None,
+                   amplifier: int = 1, stream=None) -> "PackedWeight":
+        """Pack reference int16 codes (K x N, row-major)."""
+        codes = _cuda(codes, torch.int16)
+        k, n = codes.shape
+        s, ks = cls._scales(scales, int_scales, codes.device)
+        h = C.c_void_p()
+        check(load().isb_weight_pack_codes(_ptr(codes), k, n, group, _ptr(s), _ptr(ks),
+                                           int(amplifier), _stream(stream), C.byref(h)))
+        return cls(h, codes.device)
+
+    @classmethod
+    def from_signed4(cls, data: torch.Tensor, k: int, n: int, group: int, scales,
+                     int_scales=None, amplifier: int = 1, stream=None) -> "PackedWeight":
+        """Pack the reference packed_signed4 byte stream (tensor_io.cpp:179-193)."""
+        data = _cuda(data, torch.uint8)
+        s, ks = cls._scales(scales, int_scales, data.device)
+        h = C.c_void_p()
+        check(load().isb_weight_pack_signed4(_ptr(data), data.numel(), k, n, group, _ptr(s),
+                                             _ptr(ks), int(amplifier), _stream(stream),
+                                             C.byref(h)))
+        return cls(h, data.device)
+
+    def unpack_codes(self, stream=None) -> torch.Tensor:
+        out = torch.empty((self.k, self.n), dtype=torch.int16, device=self.device)
+        check(load().isb_weight_unpack_codes(self._h, _ptr(out), _stream(stream)))
+        return out
+
+    def repack_signed4(self, stream=None) -> torch.Tensor:
+        out = torch.empty(((self.k * self.n + 1) // 2,), dtype=torch.uint8, device=self.device)
+        check(load().isb_weight_repack_signed4(self._h, _ptr(out), _stream(stream)))
+        return out
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            load().isb_weight_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------- workspace
+class Workspace:
+    """Caller-owned GEMM workspace (tile counters + split partials). Zeroed once;
+    the kernels leave it zeroed."""
+
+    def __init__(self, device=None):
+        self.device = device
+        self.buf = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = torch.zeros((max(nbytes, 256),), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_default_ws: dict = {}
+
+
+def workspace_size(m: int, w: PackedWeight) -> int:
+    b = C.c_int64()
+    check(load().isb_gemm_workspace_size(m, w.handle, C.byref(b)))
+    return b.value
+
+
+def _ws_for(m, w, workspace):
+    need = workspace_size(m, w)
+    if workspace is None:
+        key = (w.device, torch.cuda.current_stream(w.device).cuda_stream)
+        workspace = _default_ws.setdefault(key, Workspace())
+    return workspace.get(need, w.device), need
+
+
+# ---------------------------------------------------------------------------- K3 / K4
+def _gemm(path, xq, sa, w: PackedWeight, out_dtype, out, workspace, stream):
+    xq = _cuda(xq, torch.int8)
+    sa = _cuda(sa, torch.float64)
+    m, k = xq.shape
+    if out is None:
+        out = torch.empty((m, w.n), dtype=out_dtype, device=xq.device)
+    ws, need = _ws_for(m, w, workspace)
+    fn = load().isb_gemm_integer_scale if path == ISB_PATH_INTEGER_SCALE else \
+        load().isb_gemm_float_scale
+    check(fn(_ptr(xq), _ptr(sa), m, k, w.handle, _ptr(out), _DT[out.dtype], _ptr(ws), ws.numel(),
+             _stream(stream)))
+    return out
+
+
+def gemm_integer_scale(xq, sa, w: PackedWeight, out_dtype=torch.bfloat16, out=None,
+                       workspace=None, stream=None):
+    """K3 — gemm_integer_scale (gemm.cpp:205-262) on tcgen05."""
+    return _gemm(ISB_PATH_INTEGER_SCALE, xq, sa, w, out_dtype, out, workspace, stream)
+
+
+def gemm_float_scale(xq, sa, w: PackedWeight, out_dtype=torch.bfloat16, out=None,
+                     workspace=None, stream=None):
+    """K4 — gemm_float_scale (gemm.cpp:156-203), fp32 I2F+FFMA per group, on tcgen05."""
+    return _gemm(ISB_PATH_FLOAT_SCALE, xq, sa, w, out_dtype, out, workspace, stream)
+
+
+def gemm_checked(path: str, xq, sa, w: PackedWeight, strict=False, want_f64=True, want_acc=True,
+                 want_partials=False, stream=None):
+    """Checked int64 GEMM with full reference stats semantics. Returns
+    (out f32, out_f64, acc int64, partials int64, stats dict)."""
+    xq = _cuda(xq, torch.int8)
+    sa = _cuda(sa, torch.float64)
+    m, k = xq.shape
+    dev = xq.device
+    p = ISB_PATH_INTEGER_SCALE if path == "integer-scale" else ISB_PATH_FLOAT_SCALE
+    out = torch.empty((m, w.n), dtype=torch.float32, device=dev)
+    of = torch.empty((m, w.n), dtype=torch.float64, device=dev) if want_f64 else None
+    acc = torch.empty((m, w.n), dtype=torch.int64, device=dev) if want_acc and p else None
+    part = (torch.empty((m, w.n * (w.k // w.group)), dtype=torch.int64, device=dev)
+            if want_partials else None)
+    st = GemmStats()
+    check(load().isb_gemm_checked(p, _ptr(xq), _ptr(sa), m, k, w.handle, int(strict), _ptr(out),
+                                  _ptr(of), _ptr(acc), _ptr(part), C.byref(st), _stream(stream)))
+    stats = {f: getattr(st, f) for f, _ in GemmStats._fields_}
+    return out, of, acc, part, stats
+
+
+def launch_count() -> int:
+    return load().isb_launch_count()

@@ -1,0 +1,230 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle on
+identical inputs. Integer/byte work must be bit-exact; the integer-scale float32
+output is bit-exact (0 ULP); bf16/fp16 outputs equal the host-rounded oracle
+float32; the float-scale (fp32 Atom-style) variant is within a stated tolerance.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from tests.instances import llama_problem, make_w, make_x, overflow_rig, random_instance
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU, skipped there
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2405_14597_b200 as isb  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(DEV)
+
+
+def pack(w: O.QuantizedTensor, s: O.IntegerScaleSet | None):
+    return isb.PackedWeight.from_codes(
+        dev(w.values), w.group if w.kind == O.GROUP else w.rows, dev(w.scales),
+        None if s is None else dev(s.int_scales), 1 if s is None else s.amplifier)
+
+
+def to_bf16_np(f32: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(f32).to(torch.bfloat16).float().numpy()
+
+
+# ------------------------------------------------------------------------- K1
+@pytest.mark.parametrize("m,k", [(1, 4096), (16, 4096), (3, 256), (64, 11008), (5, 14336),
+                                 (2, 28672), (7, 100), (4, 4)])
+def test_quantize_per_token_bit_exact(m, k):
+    xf = O.generate_gaussian(m, k, 1.0, 43 + m + k)
+    xf[0, :] = 0.0 if m > 2 else xf[0, :]          # an all-zero row => s = 1
+    ref = O.quantize_per_token(xf)
+    codes, scales = isb.quantize_per_token(dev(xf), check_finite=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(codes.cpu().numpy().astype(np.int16), ref.values)
+    assert np.array_equal(scales.cpu().numpy(), ref.scales)          # doubles, bitwise
+
+
+def test_quantize_ties_and_extremes():
+    # exact ties: amax = 127 makes s = 1 and x/s = x, so +-0.5, 2.5, -3.5 are ties
+    x = np.array([[127.0, 0.5, -0.5, 2.5, -3.5, 126.5, -126.5, 0.0]], np.float32)
+    ref = O.quantize_per_token(x)
+    codes, scales = isb.quantize_per_token(dev(x))
+    assert codes.cpu().numpy().astype(np.int16).tolist() == ref.values.tolist()
+    assert ref.values.tolist() == [[127, 1, -1, 3, -4, 127, -127, 0]]
+    # per-token pins, test_quantize.cpp:330-339
+    x = np.array([[1.0, -2.0], [0.5, 0.25], [0.0, 0.0]], np.float32)
+    codes, scales = isb.quantize_per_token(dev(x))
+    assert scales.cpu().numpy().tolist() == [2.0 / 127.0, 0.5 / 127.0, 1.0]
+    assert codes.cpu().numpy()[0, 1] == -127
+
+
+def test_quantize_bf16_input_matches_float_of_bf16():
+    xf = O.generate_gaussian(8, 4096, 1.0, 5)
+    xb = torch.from_numpy(xf).to(torch.bfloat16)
+    ref = O.quantize_per_token(xb.float().numpy())
+    codes, scales = isb.quantize_per_token(xb.to(DEV))
+    assert np.array_equal(codes.cpu().numpy().astype(np.int16), ref.values)
+    assert np.array_equal(scales.cpu().numpy(), ref.scales)
+
+
+def test_quantize_rejects_non_finite():
+    x = np.ones((2, 64), np.float32)
+    x[1, 3] = np.nan
+    with pytest.raises(isb.ValueError_):
+        isb.quantize_per_token(dev(x), check_finite=True)
+
+
+def test_weight_group_quantizer_bit_exact():
+    wf = O.generate_llama_like(512, 300, 7)
+    ref = O.quantize_weight(wf, 128)
+    codes, scales = isb.quantize_weight(dev(wf), 128, 4)
+    assert np.array_equal(codes.cpu().numpy(), ref.values)
+    assert np.array_equal(scales.cpu().numpy(), ref.scales)
+
+
+# ------------------------------------------------------------------------- K2
+@pytest.mark.parametrize("k,n", [(256, 128), (4096, 300), (384, 1), (130, 7), (8, 2)])
+def test_pack_roundtrip_and_reference_bytes(k, n):
+    rng = O.Rng(k * 1000 + n)
+    codes = (rng.below(16, k * n) - 8).astype(np.int16).reshape(k, n)
+    g = 2 if k % 128 else 128
+    scales = np.full(n * (k // g), 0.01)
+    w = isb.PackedWeight.from_codes(dev(codes), g, dev(scales))
+    assert np.array_equal(w.unpack_codes().cpu().numpy(), codes)
+    assert np.array_equal(w.repack_signed4().cpu().numpy(), O.pack_signed4(codes))
+    # and from the reference byte stream
+    w2 = isb.PackedWeight.from_signed4(dev(O.pack_signed4(codes)), k, n, g, dev(scales))
+    assert np.array_equal(w2.unpack_codes().cpu().numpy(), codes)
+
+
+def test_pack_rejects_out_of_range_and_bad_length():
+    codes = np.zeros((128, 4), np.int16)
+    codes[3, 1] = 8
+    with pytest.raises(isb.ValueError_):
+        isb.PackedWeight.from_codes(dev(codes), 128, dev(np.ones(4)))
+    with pytest.raises(isb.LengthError):
+        isb.PackedWeight.from_signed4(dev(np.zeros(3, np.uint8)), 2, 4, 2, dev(np.ones(4)))
+
+
+# ------------------------------------------------------------------------- K3 / K4
+SHAPES = [(1, 4096, 4096), (2, 256, 4), (8, 256, 300), (16, 4096, 4096), (16, 11008, 512),
+          (33, 1024, 640), (64, 2048, 1024), (100, 512, 256), (128, 4096, 512),
+          (300, 1024, 384)]
+
+
+@pytest.mark.parametrize("m,k,n", SHAPES)
+def test_integer_scale_bit_exact(m, k, n):
+    x, w, s, _, _ = llama_problem(m, k, n, seed_w=42 + n, seed_x=43 + m)
+    ref = O.gemm_integer_scale(x, w, s)
+    pw = pack(w, s)
+    xq, sa = dev(x.values, torch.int8), dev(x.scales)
+    out32 = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.float32)
+    outbf = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    got = out32.cpu().numpy()
+    assert np.array_equal(got.view(np.int32), ref.output.view(np.int32)), \
+        f"max ulp {O.ulp_distance(got, ref.output).max()}"
+    assert np.array_equal(outbf.float().cpu().numpy(), to_bf16_np(ref.output))
+
+
+@pytest.mark.parametrize("m,k,n", SHAPES)
+def test_float_scale_within_tolerance(m, k, n):
+    x, w, s, _, _ = llama_problem(m, k, n, seed_w=42 + n, seed_x=43 + m)
+    ref = O.gemm_float_scale(x, w)
+    pw = pack(w, s)
+    out = isb.gemm_float_scale(dev(x.values, torch.int8), dev(x.scales), pw,
+                               out_dtype=torch.float32).cpu().numpy().astype(np.float64)
+    # fp32 accumulation of K/g terms vs the reference's double: |err| <= G * 2^-23 * sum|terms|
+    groups = k // 128
+    scale_abs = np.abs(ref.partials).reshape(m, n, groups) * w.scales.reshape(n, groups)[None]
+    bound = 2.0 * groups * 2.0 ** -23 * scale_abs.sum(axis=2) * x.scales[:, None] + 1e-30
+    assert (np.abs(out - ref.output_f64) <= bound).all()
+
+
+def test_integer_scale_alpha_8192_general_epilogue():
+    # alpha = 8192 puts k_g up to ~124 (outside the k<=16 fold band)
+    x, w, _, _, _ = llama_problem(16, 4096, 1024, amp=1024)
+    s = O.integerize_scales(w.scales, 8192)
+    assert s.int_scales.max() > 16
+    assert O.overflow_analyzer(4096, 128, 8, 4, s)["safe"]
+    ref = O.gemm_integer_scale(x, w, s)
+    out = isb.gemm_integer_scale(dev(x.values, torch.int8), dev(x.scales), pack(w, s),
+                                 out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(out.view(np.int32), ref.output.view(np.int32))
+
+
+def test_random_instances_vs_oracle_tensor_core():
+    rng = O.Rng(2718)
+    for _ in range(20):
+        m = 1 + rng.below(40)
+        n = 1 + rng.below(300)
+        k = 128 * (1 + rng.below(6))
+        g = [128, k][rng.below(2)]
+        x, w, _, _ = random_instance(rng, m, k, n, g)
+        amp = O.search_amplifier(w.scales)
+        s = O.integerize_scales(w.scales, amp)
+        if not O.overflow_analyzer(k, g, 8, 4, s)["safe"]:
+            continue
+        ref = O.gemm_integer_scale(x, w, s)
+        out = isb.gemm_integer_scale(dev(x.values, torch.int8), dev(x.scales), pack(w, s),
+                                     out_dtype=torch.float32).cpu().numpy()
+        assert np.array_equal(out.view(np.int32), ref.output.view(np.int32))
+
+
+def test_workspace_is_left_clean_and_results_repeat():
+    x, w, s, _, _ = llama_problem(16, 4096, 4096)
+    pw = pack(w, s)
+    xq, sa = dev(x.values, torch.int8), dev(x.scales)
+    ws = isb.Workspace()
+    a = isb.gemm_integer_scale(xq, sa, pw, torch.float32, workspace=ws)
+    for _ in range(5):
+        b = isb.gemm_integer_scale(xq, sa, pw, torch.float32, workspace=ws)
+        assert torch.equal(a, b)
+    torch.cuda.synchronize()
+    assert int(ws.buf[:1024].to(torch.int32).abs().sum()) == 0  # counters reset
+
+
+# ------------------------------------------------------------------------- checked kernel
+def test_checked_matches_oracle_stats_small_groups():
+    rng = O.Rng(1007)
+    for _ in range(30):
+        m = 1 + rng.below(8)
+        n = 1 + rng.below(8)
+        k = 4 * (1 + rng.below(8))
+        g = [1, 2, 4, k][rng.below(4)]
+        x, w, _, _ = random_instance(rng, m, k, n, g)
+        amp = O.search_amplifier(w.scales)
+        s = O.integerize_scales(w.scales, amp)
+        pw = pack(w, s)
+        xq, sa = dev(x.values, torch.int8), dev(x.scales)
+        ri = O.gemm_integer_scale(x, w, s)
+        out, of, acc, part, st = isb.gemm_checked("integer-scale", xq, sa, pw, want_partials=True)
+        assert np.array_equal(out.cpu().numpy().view(np.int32), ri.output.view(np.int32))
+        assert np.array_equal(acc.cpu().numpy(), ri.acc)
+        assert np.array_equal(part.cpu().numpy(), ri.partials)
+        assert st["max_abs_accumulator"] == ri.stats["max_abs_accumulator"]
+        rf = O.gemm_float_scale(x, w)
+        out, of, _, _, st = isb.gemm_checked("float-scale", xq, sa, pw)
+        assert np.array_equal(out.cpu().numpy().view(np.int32), rf.output.view(np.int32))
+        assert np.array_equal(of.cpu().numpy(), rf.output_f64)
+        assert st["max_abs_accumulator"] == rf.stats["max_abs_accumulator"]
+
+
+def test_checked_overflow_rig():
+    x, w, s = overflow_rig(2)
+    pw = pack(w, s)
+    xq, sa = dev(x.values, torch.int8), dev(x.scales)
+    out, of, acc, _, st = isb.gemm_checked("integer-scale", xq, sa, pw)
+    assert st["overflow_detected"] and st["max_abs_accumulator"] == 4260372480
+    assert (st["overflow_i"], st["overflow_j"]) == (0, 0)
+    assert acc.cpu().numpy()[0, 0] == -4260372480        # permissive: non-wrapped int64
+    ref = O.gemm_integer_scale(x, w, s)
+    assert np.array_equal(out.cpu().numpy().view(np.int32), ref.output.view(np.int32))
+    with pytest.raises(isb.OverflowError_, match=r"\(0, 0\)"):
+        isb.gemm_checked("integer-scale", xq, sa, pw, strict=True)
