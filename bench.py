@@ -1,0 +1,486 @@
+#!/usr/bin/env python3
+"""Benchmark: integer-scale W4A8 fine-grained GEMM on B200 (BASELINE.json metric
+"W4A8 IntScale GEMM TOPS & µs/layer vs roofline; speedup vs float-scale").
+
+Workload (BASELINE.json configs[1]): the LLaMA-2-7B linear layers of one decoder
+layer at decode M=16 tokens (q/k/v fused 4096->12288, o 4096->4096, gate/up fused
+4096->22016, down 11008->4096), group 128, alpha 1024. One step = the hot path
+over one layer: K1 per-token int8 quantize of each layer input + K3 integer-scale
+GEMM per linear. Weights are rotated over 3 layer replicas (3 x 107.5 MB > 2 x
+126 MB L2) so each step streams its weights from HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "W4A8 IntScale GEMM TOPS & µs/layer vs roofline; speedup vs float-scale"
+GROUP = 128
+ALPHA = 1024
+# LLaMA-2-7B decoder-layer linears (K, N), q/k/v and gate/up fused.
+LAYER = [("qkv_proj", 4096, 12288), ("o_proj", 4096, 4096), ("gate_up_proj", 4096, 22016),
+         ("down_proj", 11008, 4096)]
+REPLICAS = 3
+
+
+def alg_bytes(m, k, n, x_b=1, o_b=2):
+    """SURVEY §8d / BASELINE.md: N*K/2 + 4*N*K/g + M*K*x_b + 8*M + M*N*o_b."""
+    return n * k // 2 + 4 * n * k // GROUP + m * k * x_b + 8 * m + m * n * o_b
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML while the timed region runs."""
+
+    def __init__(self, index=0, period=0.05):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            names = {
+                "sw_power_cap": N.nvmlClocksThrottleReasonSwPowerCap,
+                "hw_slowdown": N.nvmlClocksThrottleReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksThrottleReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksThrottleReasonSwThermalSlowdown,
+                "hw_power_brake_slowdown": N.nvmlClocksThrottleReasonHwPowerBrakeSlowdown,
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                        r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                        for k, bit in names.items():
+                            if r & bit:
+                                self.reasons.add(k)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._t = None
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- dist
+def init_dist():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, ws):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- data
+def llama_like_weight(k, n, gen, dev):
+    """Device synthetic weight with the reference llama_like structure
+    (tensor_io.cpp:101-122): per (column, group of 128) a scale 2^u with
+    u ~ U(-9.99, -6.05), values uniform in +-0.97*7*2^u and one anchor at +-7*2^u,
+    so 4-bit group scales land in [2^-10, 2^-6] and alpha=1024 gives k_g in [1, 15]."""
+    import torch
+    g = k // GROUP
+    u = -9.99 + (-6.05 + 9.99) * torch.rand((g, n), generator=gen, device=dev, dtype=torch.float64)
+    vmax = (7.0 * torch.exp2(u)).float()                                    # [g, n]
+    w = (2.0 * torch.rand((g, GROUP, n), generator=gen, device=dev) - 1.0) * 0.97 * vmax[:, None]
+    anchor = torch.randint(0, GROUP, (g, n), generator=gen, device=dev)
+    sign = torch.where(torch.rand((g, n), generator=gen, device=dev) < 0.5, -1.0, 1.0)
+    w.scatter_(1, anchor[:, None, :], (sign * vmax)[:, None, :])
+    return w.reshape(k, n).contiguous()
+
+
+def build_layers(isb, m, dev, seed):
+    import torch
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    layers = []
+    for _ in range(REPLICAS):
+        lin = []
+        for name, k, n in LAYER:
+            wf = llama_like_weight(k, n, gen, dev)
+            codes, scales = isb.quantize_weight(wf, GROUP, 4)          # device group quantizer
+            del wf
+            s = isb.integerize_scales(scales.cpu().numpy(), ALPHA)      # offline, host
+            w = isb.PackedWeight.from_codes(codes, GROUP, scales, s.int_scales, ALPHA)
+            del codes
+            lin.append((name, k, n, w, int(s.int_scales.max())))
+        layers.append(lin)
+    xs = [torch.randn((m, k), generator=gen, device=dev, dtype=torch.float32) for _, k, _ in LAYER]
+    return layers, xs
+
+
+# ----------------------------------------------------------------------------- ours
+class LayerStep:
+    """One step: K1 quantize + K3 (or K4) GEMM per linear of one layer replica.
+    Captured into a CUDA graph per replica (8 kernel nodes)."""
+
+    def __init__(self, isb, layers, xs, m, path, dev):
+        import torch
+        self.isb, self.layers, self.xs, self.m, self.path = isb, layers, xs, m, path
+        self.q = [torch.empty((m, k), dtype=torch.int8, device=dev) for _, k, _ in LAYER]
+        self.sa = [torch.empty((m,), dtype=torch.float64, device=dev) for _ in LAYER]
+        self.out = [torch.empty((m, n), dtype=torch.bfloat16, device=dev) for _, _, n in LAYER]
+        self.ws = [isb.Workspace() for _ in range(REPLICAS)]
+        self.graphs = []
+        self.kernels_per_step = 2 * len(LAYER)
+
+    def run_eager(self, r):
+        isb = self.isb
+        gemm = isb.gemm_integer_scale if self.path == "int" else isb.gemm_float_scale
+        for i, (_, k, n, w, _) in enumerate(self.layers[r]):
+            q, sa = self.q[i], self.sa[i]
+            isb.quantize_per_token(self.xs[i], codes=q, scales=sa)
+            gemm(q, sa, w, out=self.out[i], workspace=self.ws[r])
+
+    def capture(self):
+        import torch
+        for r in range(REPLICAS):
+            self.run_eager(r)
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for r in range(REPLICAS):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    self.run_eager(r)
+                self.graphs.append(g)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+
+    def replay(self, step):
+        self.graphs[step % REPLICAS].replay()
+
+
+def time_steps(fn, steps, warmup, ws):
+    import torch
+    for i in range(warmup):
+        fn(i)
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for i in range(steps):
+        fn(warmup + i)
+    end.record()
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    return start.elapsed_time(end)  # ms
+
+
+def gemm_kernel_timing(isb, layers, xq_sa, m, path, iters=30):
+    """Average device duration of each K3 (or K4) launch, timed with CUDA events on
+    the launching stream over back-to-back launches rotating the weight replicas
+    (weights stream from HBM)."""
+    import torch
+    gemm = isb.gemm_integer_scale if path == "int" else isb.gemm_float_scale
+    res = []
+    wsp = isb.Workspace()
+    for i, (name, k, n) in enumerate(LAYER):
+        q, sa = xq_sa[i]
+        out = torch.empty((m, n), dtype=torch.bfloat16, device=q.device)
+        for r in range(REPLICAS):
+            gemm(q, sa, layers[r][i][3], out=out, workspace=wsp)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for it in range(iters):
+            gemm(q, sa, layers[it % REPLICAS][i][3], out=out, workspace=wsp)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1000.0 / iters
+        res.append({"linear": name, "M": m, "K": k, "N": n, "us": round(us, 3),
+                    "alg_bytes": alg_bytes(m, k, n), "gbps": round(alg_bytes(m, k, n) / us / 1e3, 1),
+                    "tops": round(2.0 * m * n * k / us / 1e6, 2)})
+    return res
+
+
+def run_ours(args, ws, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_2405_14597_b200 as isb
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    m = args.m
+    layers, xs = build_layers(isb, m, dev, seed=1234 + rank)
+    max_k = max(l[4] for lin in layers for l in lin)
+    ops_per_step = sum(2 * m * k * n for _, k, n in LAYER)
+
+    # ---- headline: graph-captured layer steps (K1 + K3 per linear)
+    step = LayerStep(isb, layers, xs, m, "int", dev)
+    step.capture()
+    with ClockSampler(local) as clk:
+        ms = time_steps(step.replay, args.steps, args.warmup, ws)
+    ms = max_over_ranks(ms, ws)
+    ms_per_step = ms / args.steps
+    value = ws * ops_per_step / (ms_per_step * 1e-3) / 1e12  # TOPS, whole job
+
+    # ---- float-scale denominator, identical structure
+    fstep = LayerStep(isb, layers, xs, m, "float", dev)
+    fstep.capture()
+    fms = max_over_ranks(time_steps(fstep.replay, args.steps, args.warmup, ws), ws) / args.steps
+
+    # ---- e2e: host pinned X in, host bf16 out, through the public API every step
+    xh = [x.cpu().pin_memory() for x in xs]
+    oh = [torch.empty((m, n), dtype=torch.bfloat16).pin_memory() for _, _, n in LAYER]
+    xd = [torch.empty_like(x) for x in xs]
+    e2e_ws = [isb.Workspace() for _ in range(REPLICAS)]
+
+    def e2e_step(i):
+        r = i % REPLICAS
+        for j, (_, k, n, w, _) in enumerate(layers[r]):
+            xd[j].copy_(xh[j], non_blocking=True)
+            q, sa = isb.quantize_per_token(xd[j])
+            out = isb.gemm_integer_scale(q, sa, w, workspace=e2e_ws[r])
+            oh[j].copy_(out, non_blocking=True)
+
+    e2e_ms = max_over_ranks(time_steps(e2e_step, args.steps, args.warmup, ws), ws) / args.steps
+    h2d = sum(m * k * 4 for _, k, _ in LAYER)
+    d2h = sum(m * n * 2 for _, _, n in LAYER)
+
+    # ---- dominant kernel roofline (K3), events on the launching stream
+    xq_sa = [isb.quantize_per_token(x) for x in xs]
+    kt = gemm_kernel_timing(isb, layers, xq_sa, m, "int")
+    kf = gemm_kernel_timing(isb, layers, xq_sa, m, "float")
+    tot_bytes = sum(r["alg_bytes"] for r in kt)
+    tot_us = sum(r["us"] for r in kt)
+    peak, peak_kind = load_peaks()
+    achieved = tot_bytes / tot_us / 1e3  # GB/s
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k3_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get("bytes_per_launch_decode_m16")
+        except Exception:
+            traffic = None
+
+    # ---- prefill / decode sweep of the whole layer (kernel-only, int vs float)
+    sweep = []
+    if not args.no_sweep:
+        for mm in args.sweep:
+            lay = layers
+            xq = [isb.quantize_per_token(torch.randn((mm, k), device=dev)) for _, k, _ in LAYER]
+            ti = gemm_kernel_timing(isb, lay, xq, mm, "int", iters=10)
+            tf = gemm_kernel_timing(isb, lay, xq, mm, "float", iters=10)
+            us_i = sum(r["us"] for r in ti)
+            us_f = sum(r["us"] for r in tf)
+            ops = sum(2 * mm * k * n for _, k, n in LAYER)
+            byts = sum(r["alg_bytes"] for r in ti)
+            sweep.append({"M": mm, "us_per_layer_int": round(us_i, 2),
+                          "us_per_layer_float": round(us_f, 2),
+                          "speedup_vs_float": round(us_f / us_i, 3),
+                          "tops_int": round(ops / us_i / 1e6, 1),
+                          "hbm_frac_int": round(byts / us_i / 1e3 / peak, 3)})
+
+    result = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "TOPS",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 5),
+        "us_per_layer": round(ms_per_step * 1e3, 2),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int8 (s8 x s4->s8 MMA, s32 accumulate)",
+        "data": "synthetic (llama_like-structured int4 weights, gaussian activations; device-generated)",
+        "config": {
+            "workload": f"llama2-7b decoder-layer linears, decode M={m}",
+            "M": m, "linears": [{"name": a, "K": k, "N": n} for a, k, n in LAYER],
+            "group": GROUP, "alpha": ALPHA, "max_int_scale": max_k,
+            "step": "K1 per-token quantize + K3 integer-scale GEMM per linear (8 kernels, CUDA graph)",
+            "l2": f"weights rotated over {REPLICAS} layer replicas ({REPLICAS}x107.5MB > 2x126MB L2)",
+            "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+        },
+        "speedup_vs_float_scale": round(fms / ms_per_step, 3),
+        "float_scale_us_per_layer": round(fms * 1e3, 2),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "kernel": "gemm_w4a8_tc<MT=16, integer-scale>",
+                     "alg_bytes_per_layer": tot_bytes, "kernel_us_per_layer": round(tot_us, 2),
+                     "per_linear": kt},
+        "float_scale_kernel": kf,
+        "e2e": {"value": round(ws * ops_per_step / (e2e_ms * 1e-3) / 1e12, 3), "unit": "TOPS",
+                "us_per_layer": round(e2e_ms * 1e3, 2),
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": args.steps * step.kernels_per_step,
+        "clocks": clk.summary(),
+        "sweep": sweep,
+    }
+    return result
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def cpu_layer_sample(m, threads, repeats=1, seed=42):
+    """The oracle (CPU restatement of gemm_integer_scale, gemm.cpp:205-262) on one
+    LLaMA-2-7B layer at M rows, reference-style row-partitioned std::threads.
+    Returns (TOPS, seconds per layer)."""
+    from oracle import oracle as O
+    probs = []
+    for i, (_, k, n) in enumerate(LAYER):
+        w = O.quantize_weight(O.generate_llama_like(k, n, seed + i), GROUP)
+        x = O.quantize_per_token(O.generate_gaussian(m, k, 1.0, seed + 100 + i))
+        s = O.integerize_scales(w.scales, ALPHA)
+        probs.append((x, w, s))
+    times = []
+    for _ in range(repeats):
+        t = 0.0
+        for x, w, s in probs:
+            r = O.gemm_integer_scale(x, w, s, workers=threads, record=False)
+            t += r.stats["wall_ms"] / 1e3
+        times.append(t)
+    sec = statistics.median(times)
+    ops = sum(2 * m * k * n for _, k, n in LAYER)
+    return ops / sec / 1e12, sec, probs
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference path's CPU implementation (the oracle port;
+    the reference itself cannot be built here) on this box's host cores."""
+    if rank != 0:
+        return None
+    threads = min(os.cpu_count() or 1, args.m)  # the reference parallelises over rows only
+    from oracle import oracle as O
+    _, _, probs = cpu_layer_sample(args.m, threads, repeats=0)
+    per_step = []
+    for i in range(args.warmup + args.steps):
+        t = 0.0
+        for x, w, s in probs:
+            t += O.gemm_integer_scale(x, w, s, workers=threads, record=False).stats["wall_ms"] / 1e3
+        if i >= args.warmup:
+            per_step.append(t)
+    sec = sum(per_step) / len(per_step)
+    ops = sum(2 * args.m * k * n for _, k, n in LAYER)
+    v = ops / sec / 1e12
+    sample = (f"one LLaMA-2-7B decoder layer's linears at M={args.m} per step "
+              f"(oracle port of gemm_integer_scale, {threads} row-partitioned threads)")
+    return {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "TOPS", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "us_per_layer": sec * 1e6, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64 (CPU int16 codes, int64 accumulate)",
+        "data": "synthetic (reference generators: llama_like W seed 42+i, gaussian X)",
+        "config": {"workload": f"llama2-7b decoder-layer linears, decode M={args.m}", "M": args.m,
+                   "linears": [{"name": a, "K": k, "N": n} for a, k, n in LAYER],
+                   "group": GROUP, "alpha": ALPHA},
+        "cpu_baseline": {"value": v, "unit": "TOPS", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def cpu_baseline(args):
+    threads = min(os.cpu_count() or 1, args.m)
+    tops, sec, _ = cpu_layer_sample(args.m, threads, repeats=3)
+    try:
+        model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo")
+                     if l.startswith("model name"))
+    except Exception:
+        model = "unknown"
+    return {"value": tops, "unit": "TOPS", "cores": threads, "kind": "port",
+            "sample": (f"one LLaMA-2-7B layer's 4 linears at M={args.m}, median of 3 "
+                       f"({sec * 1e3:.0f} ms/layer); oracle port of gemm_integer_scale, "
+                       f"{threads} row-partitioned threads of {os.cpu_count()} on {model}; "
+                       f"-O3 -DNDEBUG -ffp-contract=off")}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--m", type=int, default=16)
+    ap.add_argument("--sweep", type=int, nargs="*", default=[1, 16, 64, 2048])
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        ws = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        res = run_reference(args, ws, rank)
+        if res is not None:
+            print(json.dumps(res))
+        return
+
+    ws, rank, local = init_dist()
+    res = run_ours(args, ws, rank, local)
+    if rank == 0:
+        if ws == 1 and not args.no_cpu:
+            res["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(res))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

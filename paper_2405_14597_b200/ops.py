@@ -38,17 +38,20 @@ def _cuda(t, dtype=None):
 
 
 # ---------------------------------------------------------------------------- K1
-def quantize_per_token(x: torch.Tensor, check_finite: bool = False, stream=None):
+def quantize_per_token(x: torch.Tensor, check_finite: bool = False, stream=None, codes=None,
+                       scales=None):
     """quantize(x, 8, symmetric, per_token) — quantize.cpp:93-145. Returns
-    (codes int8 [M, K], scales float64 [M])."""
+    (codes int8 [M, K], scales float64 [M]); `codes`/`scales` may be preallocated."""
     x = _cuda(x)
     if x.dtype not in (torch.float32, torch.bfloat16):
         raise _lib.ParamError("activations must be float32 or bfloat16")
     if x.dim() != 2:
         raise _lib.ParamError("activations must be 2-d")
     m, k = x.shape
-    codes = torch.empty((m, k), dtype=torch.int8, device=x.device)
-    scales = torch.empty((m,), dtype=torch.float64, device=x.device)
+    if codes is None:
+        codes = torch.empty((m, k), dtype=torch.int8, device=x.device)
+    if scales is None:
+        scales = torch.empty((m,), dtype=torch.float64, device=x.device)
     check(load().isb_quantize_per_token(_ptr(x), _DT[x.dtype], m, k, _ptr(codes), _ptr(scales),
                                         int(check_finite), _stream(stream)))
     return codes, scales
