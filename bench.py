@@ -53,7 +53,7 @@ def load_peaks():
 class ClockSampler:
     """Samples SM clock + throttle reasons via NVML while the timed region runs."""
 
-    def __init__(self, index=0, period=0.05):
+    def __init__(self, index=0, period=0.005):
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
         self._stop = threading.Event()
@@ -453,8 +453,8 @@ def cpu_baseline(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--m", type=int, default=16)
     ap.add_argument("--sweep", type=int, nargs="*", default=[1, 16, 64, 2048])
