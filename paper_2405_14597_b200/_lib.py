@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libintscale_b200.so")
+LIB_PATH = os.environ.get("ISB_LIB_PATH") or os.path.join(_HERE, "libintscale_b200.so")
 
 ISB_OK, ISB_PARAM, ISB_DIMENSION, ISB_VALUE, ISB_OVERFLOW, ISB_LENGTH, ISB_FORMAT, ISB_ERROR, \
     ISB_CUDA = range(9)

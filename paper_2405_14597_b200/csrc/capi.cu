@@ -177,7 +177,7 @@ void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
     fail(ISB_PARAM, "integer-scale path needs an IntegerScaleSet");
   if (m > std::numeric_limits<int>::max() || w->n > std::numeric_limits<int>::max())
     fail(ISB_PARAM, "shape too large");
-  const GemmPlan pl = plan_gemm(m, *w, num_sms());
+  const GemmPlan pl = plan_gemm(m, *w, num_sms(), path);
   if (!ws || ws_bytes < pl.workspace_bytes)
     fail(ISB_PARAM, "workspace too small: need " + std::to_string(pl.workspace_bytes) + " bytes");
   launch_gemm_tc(path, xq, sa, m, *w, out, out_dtype, ws, pl, as_stream(stream));
@@ -299,7 +299,10 @@ int isb_gemm_workspace_size(int64_t m, const isb_weight* w, int64_t* bytes) {
   return guarded([&] {
     if (!w || !bytes) fail(ISB_PARAM, "null pointer");
     if (m < 1) fail(ISB_PARAM, "shape must be at least 1x1");
-    *bytes = w->tensor_core_ok() ? plan_gemm(m, *w, num_sms()).workspace_bytes : 0;
+    *bytes = w->tensor_core_ok()
+                 ? std::max(plan_gemm(m, *w, num_sms(), ISB_PATH_INTEGER_SCALE).workspace_bytes,
+                            plan_gemm(m, *w, num_sms(), ISB_PATH_FLOAT_SCALE).workspace_bytes)
+                 : 0;
   });
 }
 
@@ -359,6 +362,21 @@ int isb_gemm_checked(int path, const int8_t* xq, const double* sa, int64_t m, in
                              std::to_string(st.overflow_i) + ", " + std::to_string(st.overflow_j) +
                              ")");
   });
+}
+
+/* Debug: record a clock64 timeline of one CTA of subsequent tcgen05 GEMM launches
+ * into trace (device, 8 x 512 int64; roles: 0 producer issue, 1 transform data
+ * ready, 2 MMA commit, 3 transform A ready, 4 epilogue D ready, 5 producer start,
+ * 6 CTA end, 7 CTA start). trace = NULL disables. Not part of the stable ABI. */
+int isb_debug_set_trace(int64_t* trace, int cta) {
+  g_trace = trace;
+  g_trace_cta = cta;
+  return ISB_OK;
+}
+
+int isb_debug_set_flags(int flags) {
+  g_dbg = flags;
+  return ISB_OK;
 }
 
 int isb_overflow_analyzer(int64_t k, int64_t group, int act_bits, int weight_bits,

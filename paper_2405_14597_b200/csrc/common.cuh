@@ -20,6 +20,18 @@ ISB_DEVICE uint32_t smem_u32(const void* p) {
 ISB_DEVICE uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x / 32, 0); }
 ISB_DEVICE uint32_t lane_id() { return threadIdx.x & 31u; }
 
+ISB_DEVICE int64_t clock64_() {
+  int64_t t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+
+ISB_DEVICE int64_t globaltimer_() {
+  int64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 ISB_DEVICE bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -58,15 +70,25 @@ ISB_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 
 ISB_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
+#ifdef ISB_SPIN_WAIT
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@P1 bra DONE_%=;\n\t"
       "bra WAIT_%=;\n\t"
       "DONE_%=:\n\t}" ::"r"(addr),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // ----------------------------------------------------------------------------
@@ -221,6 +243,74 @@ __host__ __device__ constexpr uint32_t make_idesc_i8(uint32_t M, uint32_t N) {
          | (1u << 10)         // b_format = signed int8
          | ((N >> 3) << 17)   // n_dim
          | ((M >> 4) << 24);  // m_dim
+}
+
+}  // namespace isb
+
+namespace isb {
+
+ISB_DEVICE uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+ISB_DEVICE uint32_t ld_shared_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// Per-thread async 4-byte global -> shared copy (LDGSTS), grouped by commit.
+ISB_DEVICE void cp_async_4(uint32_t smem_addr, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr), "l"(gmem) : "memory");
+}
+ISB_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+ISB_DEVICE void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+}  // namespace isb
+
+namespace isb {
+
+// Warp-converged issue: the whole warp executes the asm, elect.sync picks one
+// lane to issue. Keeps operands in the uniform datapath (no per-instruction
+// R2UR waterfall that a `if (lane == 0)` region produces).
+ISB_DEVICE void mma_i8_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(
+          d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+      : "memory");
+}
+
+ISB_DEVICE void mma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace isb
+
+namespace isb {
+
+// Programmatic dependent launch (PDL). wait: block until the preceding grid in
+// the stream has completed and its memory is visible; launch_dependents: allow
+// the next grid to start launching (its prologue overlaps our tail).
+ISB_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+ISB_DEVICE void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 }  // namespace isb

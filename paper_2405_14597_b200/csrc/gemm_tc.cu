@@ -35,22 +35,31 @@
 namespace isb {
 namespace {
 
-constexpr int kStages = 4;
+constexpr int kPrefetch = 8;  // epilogue scale prefetch depth (groups)
 
 template <int MT>
 struct Cfg {
   static constexpr int kEpiWG = MT >= 128 ? 2 : 1;           // epilogue warpgroups
   static constexpr int kCols = MT / kEpiWG;                   // D columns per epilogue WG
-  static constexpr int kThreads = 256 + 128 * kEpiWG;
-  static constexpr int kNA = 4;                               // TMEM A stages (32 cols each)
-  static constexpr int kND = MT >= 128 ? 3 : (MT >= 64 ? 4 : (MT >= 16 ? 4 : 8));
+  static constexpr int kXformWG = MT >= 128 ? 1 : 2;          // int4->int8 transform warpgroups
+  static constexpr int kThreads = 128 + 128 * kXformWG + 128 * kEpiWG;
+  // TMEM: kNA A-operand stages (32 cols each) + kND accumulator slots (MT cols each).
+  // The A ring is a transform->MMA->transform loop whose round trip is several
+  // mbarrier hops, so it must be deep enough to cover that latency.
+  static constexpr int kNA = MT >= 128 ? 4 : 8;
+  static constexpr int kND = MT >= 128 ? 3 : (MT >= 64 ? 4 : 8);
   static constexpr int kTmemUsed = kNA * 32 + kND * MT;
   static constexpr int kTmemCols = kTmemUsed <= 32 ? 32 : kTmemUsed <= 64 ? 64
                                    : kTmemUsed <= 128 ? 128 : kTmemUsed <= 256 ? 256 : 512;
   static_assert(kTmemUsed <= 512, "TMEM overflow");
   static constexpr int kXBytes = MT * 128;
-  static constexpr int kStageBytes = kBlockBytes + kXBytes;
-  static constexpr int kSmemBytes = 1024 + kStages * (kBlockBytes + (kXBytes < 1024 ? 1024 : kXBytes)) + 512;
+  static constexpr int kXSlot = kXBytes < 1024 ? 1024 : kXBytes;
+  // Enough smem stages to cover the producer->HBM->transform->MMA->producer loop.
+  static constexpr int kStages = (196 * 1024) / (kBlockBytes + kXSlot) > 24
+                                     ? 24 : (196 * 1024) / (kBlockBytes + kXSlot);
+  static constexpr int kRingBytes = kEpiWG * kPrefetch * kTileN * 4;
+  static constexpr int kSmemBytes = 1024 + kStages * (kBlockBytes + kXSlot) + kRingBytes + 1024;
+  static_assert(kSmemBytes <= 227 * 1024, "smem budget");
 };
 
 struct Params {
@@ -64,7 +73,21 @@ struct Params {
   int M, N, G, gb, kblocks, m_tiles, tiles, maxc, out_dtype;
   int64_t units;
   double inv_amp;  // 2^-e (exact)
+  int64_t* trace;  // optional per-role clock64 timeline of CTA `trace_cta` (debug)
+  int trace_cta;
+  int dbg;         // debug knobs: 1 skip A st, 2 skip D ld, 4 skip MMA issue
 };
+
+// Debug timeline: trace[role * 512 + i] = globaltimer at event i of that role (16 roles).
+#define ISB_TRACE_CTA(role)                                                    \
+  do {                                                                         \
+    if (p.trace != nullptr) p.trace[(role) * 512 + blockIdx.x] = globaltimer_(); \
+  } while (0)
+#define ISB_TRACE(role, i)                                                              \
+  do {                                                                                  \
+    if (p.trace != nullptr && static_cast<int>(blockIdx.x) == p.trace_cta && (i) < 512) \
+      p.trace[(role) * 512 + (i)] = globaltimer_();                                         \
+  } while (0)
 
 __device__ __forceinline__ int cta_of(int64_t u, int64_t U, int P) {
   int c = static_cast<int>((u * P) / U);
@@ -89,10 +112,12 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  constexpr int kXSlot = C::kXBytes < 1024 ? 1024 : C::kXBytes;
+  constexpr int kXSlot = C::kXSlot;
+  constexpr int kStages = C::kStages;
   uint8_t* smem_w = smem;                                  // kStages x 8 KiB
   uint8_t* smem_x = smem + kStages * kBlockBytes;          // kStages x kXSlot (1 KiB aligned)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_x + kStages * kXSlot);
+  int32_t* scale_ring = reinterpret_cast<int32_t*>(smem_x + kStages * kXSlot);  // [wg][PF][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_x + kStages * kXSlot + C::kRingBytes);
   uint64_t* full = bars;
   uint64_t* empty = full + kStages;
   uint64_t* a_full = empty + kStages;
@@ -126,6 +151,9 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) ISB_TRACE(7, 0);
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  if (threadIdx.x == 0 && p.trace != nullptr) p.trace[14 * 512 + blockIdx.x] = globaltimer_();
 
   const int P = gridDim.x;
   const int64_t U = p.units;
@@ -133,78 +161,117 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
   const int64_t u1 = (static_cast<int64_t>(blockIdx.x + 1) * U) / P;
   const int G = p.G, gb = p.gb;
 
+  // Every role walks the same kblock sequence j = 0, 1, ... over this CTA's units;
+  // ring slots and mbarrier parities are pure functions of j.
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
     if (elect_one()) {
-      int stage = 0;
-      uint32_t phase = 0;
+      ISB_TRACE(5, 0);
+      // Weight blocks do not depend on the preceding kernel: stream the first
+      // kStages of them before griddepcontrol.wait so their HBM latency hides
+      // behind the previous grid's tail (PDL). Activations (X) are loaded after.
+      int j = 0;
+      bool waited = false;
+      for (int64_t u = u0; u < u1;) {
+        const int tile = static_cast<int>(u / G);
+        const int g0 = static_cast<int>(u % G);
+        const int g1 = static_cast<int>((G < g0 + (u1 - u) ? static_cast<int64_t>(G) : g0 + (u1 - u)));
+        const int nt = tile / p.m_tiles;
+        for (int kb = g0 * gb; kb < g1 * gb && j < kStages; ++kb, ++j) {
+          mbar_arrive_expect_tx(&full[j], kBlockBytes + C::kXBytes);
+          bulk_load_evict_first(smem_w + j * kBlockBytes,
+                                p.packed + (static_cast<int64_t>(nt) * p.kblocks + kb) * kBlockBytes,
+                                kBlockBytes, &full[j]);
+        }
+        if (j >= kStages) break;
+        u += g1 - g0;
+      }
+      const int prefetched = j;
+      pdl_wait();
+      waited = true;
+      (void)waited;
+      j = 0;
       for (int64_t u = u0; u < u1;) {
         const int tile = static_cast<int>(u / G);
         const int g0 = static_cast<int>(u % G);
         const int g1 = static_cast<int>((G < g0 + (u1 - u) ? static_cast<int64_t>(G) : g0 + (u1 - u)));
         const int nt = tile / p.m_tiles, mt = tile % p.m_tiles;
-        for (int kb = g0 * gb; kb < g1 * gb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], kBlockBytes + C::kXBytes);
-          bulk_load_evict_first(smem_w + stage * kBlockBytes,
-                                p.packed + (static_cast<int64_t>(nt) * p.kblocks + kb) * kBlockBytes,
-                                kBlockBytes, &full[stage]);
+        for (int kb = g0 * gb; kb < g1 * gb; ++kb, ++j) {
+          const int stage = j % kStages;
+          if (j >= prefetched) {
+            mbar_wait(&empty[stage], ((j / kStages) & 1) ^ 1);
+            ISB_TRACE(13, j);
+            mbar_arrive_expect_tx(&full[stage], kBlockBytes + C::kXBytes);
+            bulk_load_evict_first(smem_w + stage * kBlockBytes,
+                                  p.packed + (static_cast<int64_t>(nt) * p.kblocks + kb) * kBlockBytes,
+                                  kBlockBytes, &full[stage]);
+          }
           tma_load_2d(smem_x + stage * kXSlot, &x_map, &full[stage], kb * kBlockK, mt * MT);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          ISB_TRACE(0, j);
         }
         u += g1 - g0;
       }
+      ISB_TRACE_CTA(18);
     }
+    __syncwarp();
   } else if (warp == 1) {
-    // ---------------------------------------------------------------- MMA issuer
+    // ---------------------------------------------------------------- MMA issuer (whole warp)
     constexpr uint32_t idesc = make_idesc_i8(128, MT);
-    int stage = 0, as = 0, ds = 0;
-    uint32_t phase = 0, aphase = 0, dphase = 0;
+    const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint32_t x_base = smem_u32(smem_x);
+    int j = 0, gi = 0;
     for (int64_t u = u0; u < u1;) {
       const int g0 = static_cast<int>(u % G);
       const int g1 = static_cast<int>((G < g0 + (u1 - u) ? static_cast<int64_t>(G) : g0 + (u1 - u)));
-      for (int g = g0; g < g1; ++g) {
-        mbar_wait(&d_empty[ds], dphase ^ 1);
-        const uint32_t d_tmem = tmem_base + C::kNA * 32 + ds * MT;
-        for (int b = 0; b < gb; ++b) {
-          mbar_wait(&full[stage], phase);
-          mbar_wait(&a_full[as], aphase);
+      for (int g = g0; g < g1; ++g, ++gi) {
+        const int ds = gi % C::kND;
+        mbar_wait(&d_empty[ds], ((gi / C::kND) & 1) ^ 1);
+        if (lane == 0) ISB_TRACE(8, j);
+        const uint32_t d_tmem = tbase + C::kNA * 32 + ds * MT;
+        for (int b = 0; b < gb; ++b, ++j) {
+          const int stage = j % kStages, as = j % C::kNA;
+          // a_full implies full: the transform warps observed full[stage] (weights
+          // and activations of this stage) before arriving.
+          mbar_wait(&a_full[as], (j / C::kNA) & 1);
+          if (lane == 0) ISB_TRACE(10, j);
           tc_fence_after();
-          if (lane == 0) {
-            const uint64_t bdesc = make_sw128_kmajor_desc(smem_u32(smem_x + stage * kXSlot));
+          const uint64_t bdesc = make_sw128_kmajor_desc(x_base + stage * kXSlot);
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-              mma_i8_ts(d_tmem, tmem_base + as * 32 + c * 8, bdesc + static_cast<uint64_t>(c * 2),
-                        idesc, (b > 0 || c > 0) ? 1u : 0u);
-            mma_commit(&empty[stage]);
-            mma_commit(&a_empty[as]);
-            if (b == gb - 1) mma_commit(&d_full[ds]);
-          }
-          __syncwarp();
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
-          if (++as == C::kNA) { as = 0; aphase ^= 1; }
+          for (int c = 0; c < 4; ++c)
+            if (!(p.dbg & 4))
+              mma_i8_ts_warp(d_tmem, tbase + as * 32 + c * 8, bdesc + static_cast<uint64_t>(c * 2),
+                             idesc, (b > 0 || c > 0) ? 1u : 0u);
+          mma_commit_warp(&empty[stage]);
+          mma_commit_warp(&a_empty[as]);
+          if (b == gb - 1) mma_commit_warp(&d_full[ds]);
+          if (lane == 0) ISB_TRACE(2, j);
         }
-        if (++ds == C::kND) { ds = 0; dphase ^= 1; }
       }
       u += g1 - g0;
     }
-  } else if (warp >= 4 && warp < 8) {
+    if (lane == 0) ISB_TRACE_CTA(19);
+  } else if (warp >= 4 && warp < 4 + 4 * C::kXformWG) {
     // ---------------------------------------------------------------- transform
-    const uint32_t r = (warp - 4) * 32 + lane;  // output channel within the tile == TMEM lane
-    const uint32_t lane_base = ((warp - 4) * 32) << 16;
-    int stage = 0, as = 0;
-    uint32_t phase = 0, aphase = 0;
+    // kXformWG warpgroups take alternate kblocks; thread r owns output channel r.
+    const uint32_t xw = (warp - 4) / 4;
+    const uint32_t r = (warp % 4) * 32 + lane;  // == TMEM lane
+    const uint32_t lane_base = ((warp % 4) * 32) << 16;
+    const uint32_t w_base = smem_u32(smem_w) + r * 16;
+    int j = 0;
     for (int64_t u = u0; u < u1;) {
       const int g0 = static_cast<int>(u % G);
       const int g1 = static_cast<int>((G < g0 + (u1 - u) ? static_cast<int64_t>(G) : g0 + (u1 - u)));
-      for (int kb = g0 * gb; kb < g1 * gb; ++kb) {
-        mbar_wait(&full[stage], phase);
+      for (int kb = g0 * gb; kb < g1 * gb; ++kb, ++j) {
+        if (j % C::kXformWG != static_cast<int>(xw)) continue;
+        const int stage = j % kStages, as = j % C::kNA;
+        mbar_wait(&full[stage], (j / kStages) & 1);
+        if (warp == 4 && lane == 0) ISB_TRACE(1, j);
         uint4 q[4];
-        const uint8_t* src = smem_w + stage * kBlockBytes + r * 16;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) q[c] = *reinterpret_cast<const uint4*>(src + c * (kTileN * 16));
+        for (int c = 0; c < 4; ++c) q[c] = ld_shared_v4(w_base + stage * kBlockBytes + c * (kTileN * 16));
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
+        if (warp == 4 && lane == 0) ISB_TRACE(11, j);
         uint32_t a[32];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -215,21 +282,21 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
             a[c * 8 + 2 * w + 1] = w4[w] & 0xF0F0F0F0u;
           }
         }
-        mbar_wait(&a_empty[as], aphase ^ 1);
+        mbar_wait(&a_empty[as], ((j / C::kNA) & 1) ^ 1);
+        if (warp == 4 && lane == 0) ISB_TRACE(12, j);
         tc_fence_after();
-        tmem_st_x32(tmem_base + lane_base + as * 32, a);
+        if (!(p.dbg & 1)) tmem_st_x32(tmem_base + lane_base + as * 32, a);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_full[as]);
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
-        if (++as == C::kNA) { as = 0; aphase ^= 1; }
+        if (warp == 4 && lane == 0) ISB_TRACE(3, j);
       }
       u += g1 - g0;
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 4 + 4 * C::kXformWG) {
     // ---------------------------------------------------------------- epilogue
-    const uint32_t ew = warp - 8;             // 0 .. 4*kEpiWG-1
+    const uint32_t ew = warp - (4 + 4 * C::kXformWG);  // 0 .. 4*kEpiWG-1
     const uint32_t wg = ew / 4;               // which column half
     const uint32_t r = (ew % 4) * 32 + lane;  // TMEM lane == output channel in tile
     const uint32_t lane_base = ((ew % 4) * 32) << 16;
@@ -237,55 +304,94 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
     constexpr int kCols = C::kCols;
     int ds = 0;
     uint32_t dphase = 0;
+    // Per-thread async prefetch of this row's group scale kPrefetch groups ahead
+    // (the scales stream from HBM; a dependent load per group would serialise
+    // the epilogue on DRAM latency).
+    const int32_t* scale_src = PATH == ISB_PATH_INTEGER_SCALE
+                                   ? p.kscale : reinterpret_cast<const int32_t*>(p.fscale);
+    const uint32_t ring = smem_u32(scale_ring) + (wg * kPrefetch * kTileN + r) * 4;
+    auto prefetch = [&](int64_t uu) {
+      if (uu < u1) {
+        const int t = static_cast<int>(uu / G), gg = static_cast<int>(uu % G);
+        const int64_t sidx = (static_cast<int64_t>(t / p.m_tiles) * G + gg) * kTileN + r;
+        cp_async_4(ring + static_cast<uint32_t>((uu - u0) % kPrefetch) * (kTileN * 4),
+                   scale_src + sidx);
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int j = 0; j < kPrefetch; ++j) prefetch(u0 + j);
+    pdl_wait();  // sa, the workspace and the output may be touched by the previous grid
     for (int64_t u = u0; u < u1;) {
       const int tile = static_cast<int>(u / G);
       const int g0 = static_cast<int>(u % G);
-      const int g1 = static_cast<int>((G < g0 + (u1 - u) ? static_cast<int64_t>(G) : g0 + (u1 - u)));
+      const int g1 = static_cast<int>(G < g0 + (u1 - u) ? static_cast<int64_t>(G) : g0 + (u1 - u));
       const int nt = tile / p.m_tiles, mt = tile % p.m_tiles;
       int32_t iacc[kCols];
       float facc[kCols];
 #pragma unroll
       for (int t = 0; t < kCols; ++t) { iacc[t] = 0; facc[t] = 0.0f; }
       for (int g = g0; g < g1; ++g) {
-        const int64_t sidx = (static_cast<int64_t>(nt) * G + g) * kTileN + r;
-        int32_t kg = 0;
-        float sg = 0.0f;
-        if (PATH == ISB_PATH_INTEGER_SCALE) kg = __ldg(p.kscale + sidx);
-        else sg = __ldg(p.fscale + sidx);
+        const int64_t uu = u + (g - g0);
+        cp_async_wait<kPrefetch - 1>();
+        const uint32_t sraw =
+            ld_shared_u32(ring + static_cast<uint32_t>((uu - u0) % kPrefetch) * (kTileN * 4));
+        const int32_t kg = static_cast<int32_t>(sraw);
+        const float sg = __uint_as_float(sraw);
+        prefetch(uu + kPrefetch);
         mbar_wait(&d_full[ds], dphase);
+        if (ew == 0 && lane == 0) ISB_TRACE(4, static_cast<int>(uu - u0));
         tc_fence_after();
-        uint32_t v[kCols];
         const uint32_t taddr = tmem_base + lane_base + C::kNA * 32 + ds * MT + c0;
+        constexpr int kChunk = kCols < 16 ? kCols : 16;
 #pragma unroll
-        for (int c = 0; c < kCols; c += 8)
-          tmem_ld_x8(taddr + c, *reinterpret_cast<uint32_t(*)[8]>(&v[c]));
-        tmem_wait_ld();
+        for (int cc = 0; cc < kCols; cc += kChunk) {
+          uint32_t v[kChunk];
+#pragma unroll
+          for (int c = 0; c < kChunk; c += 8) {
+            if (!(p.dbg & 2)) {
+              tmem_ld_x8(taddr + cc + c, *reinterpret_cast<uint32_t(*)[8]>(&v[c]));
+            } else {
+#pragma unroll
+              for (int z = 0; z < 8; ++z) v[c + z] = z;
+            }
+          }
+          tmem_wait_ld();
+#pragma unroll
+          for (int t = 0; t < kChunk; ++t) {
+            const int32_t d = static_cast<int32_t>(v[t]);  // 16 * P_g, exact
+            if (PATH == ISB_PATH_INTEGER_SCALE)
+              iacc[cc + t] += (d >> 4) * kg;                      // Eq. 2: int32 scaled accumulation
+            else
+              facc[cc + t] = fmaf(static_cast<float>(d), sg, facc[cc + t]);  // Eq. 1, fp32
+          }
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&d_empty[ds]);
         if (++ds == C::kND) { ds = 0; dphase ^= 1; }
-#pragma unroll
-        for (int t = 0; t < kCols; ++t) {
-          const int32_t d = static_cast<int32_t>(v[t]);  // 16 * P_g, exact
-          if (PATH == ISB_PATH_INTEGER_SCALE)
-            iacc[t] += (d >> 4) * kg;                      // Eq. 2: int32 scaled accumulation
-          else
-            facc[t] = fmaf(static_cast<float>(d), sg, facc[t]);  // Eq. 1, Atom-style fp32
-        }
       }
       // ------------------------------------------------ tile completion
+      if (ew == 0 && lane == 0) ISB_TRACE_CTA(16);
       const bool whole = (g0 == 0 && g1 == G);
       bool finalize = whole;
       if (!whole) {
         const int first = cta_of(static_cast<int64_t>(tile) * G, U, P);
         const int last = cta_of(static_cast<int64_t>(tile) * G + G - 1, U, P);
         const int j = blockIdx.x - first;
-        int32_t* slice = p.partials + (static_cast<int64_t>(tile) * p.maxc + j) * MT * kTileN;
+        int32_t* tile_ws = p.partials + static_cast<int64_t>(tile) * p.maxc * MT * kTileN;
+        if (PATH == ISB_PATH_INTEGER_SCALE) {
+          // Integer partials commute: reduce in L2 with red.add (order-free, exact).
 #pragma unroll
-        for (int t = 0; t < kCols; ++t)
-          slice[(c0 + t) * kTileN + r] =
-              PATH == ISB_PATH_INTEGER_SCALE ? iacc[t] : __float_as_int(facc[t]);
+          for (int t = 0; t < kCols; ++t) atomicAdd(tile_ws + (c0 + t) * kTileN + r, iacc[t]);
+        } else {
+          int32_t* slice = tile_ws + static_cast<int64_t>(j) * MT * kTileN;
+#pragma unroll
+          for (int t = 0; t < kCols; ++t) slice[(c0 + t) * kTileN + r] = __float_as_int(facc[t]);
+        }
+        if (ew == 0 && lane == 0) ISB_TRACE_CTA(20);
         __threadfence();
+        if (ew == 0 && lane == 0) ISB_TRACE_CTA(21);
         named_bar_sync(1, 128 * C::kEpiWG);
         if (ew == 0 && lane == 0) {
           const int old = atomicAdd(p.counters + tile, 1);
@@ -296,22 +402,54 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
         named_bar_sync(1, 128 * C::kEpiWG);
         finalize = *last_flag != 0;
         named_bar_sync(1, 128 * C::kEpiWG);
+        if (ew == 0 && lane == 0) ISB_TRACE_CTA(22);
         if (finalize) {
           __threadfence();
-          const int nc = last - first + 1;
-#pragma unroll
-          for (int t = 0; t < kCols; ++t) { iacc[t] = 0; facc[t] = 0.0f; }
-          for (int jj = 0; jj < nc; ++jj) {
-            const int32_t* sl = p.partials + (static_cast<int64_t>(tile) * p.maxc + jj) * MT * kTileN;
+          if (PATH == ISB_PATH_INTEGER_SCALE) {
 #pragma unroll
             for (int t = 0; t < kCols; ++t) {
-              const int32_t x = __ldcg(sl + (c0 + t) * kTileN + r);
-              if (PATH == ISB_PATH_INTEGER_SCALE) iacc[t] += x;
-              else facc[t] += __int_as_float(x);
+              int32_t* a = tile_ws + (c0 + t) * kTileN + r;
+              iacc[t] = __ldcg(a);
+              __stcg(a, 0);  // leave the accumulator zeroed for the next launch
+            }
+          } else {
+            // Fixed-order (deterministic) fp32 reduction over the contributors,
+            // all slices of a column chunk loaded before use.
+            const int nc = last - first + 1;
+            constexpr int kMaxC = 8;
+#pragma unroll
+            for (int t0 = 0; t0 < kCols; t0 += 8) {
+              float part[kMaxC][8];
+#pragma unroll
+              for (int jj = 0; jj < kMaxC; ++jj)
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                  part[jj][t] = (jj < nc && t0 + t < kCols)
+                                    ? __int_as_float(__ldcg(tile_ws + static_cast<int64_t>(jj) * MT * kTileN +
+                                                            (c0 + t0 + t) * kTileN + r))
+                                    : 0.0f;
+              // leave the slices zeroed: the integer path red.adds into this workspace
+#pragma unroll
+              for (int jj = 0; jj < kMaxC; ++jj)
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                  if (jj < nc && t0 + t < kCols)
+                    __stcg(tile_ws + static_cast<int64_t>(jj) * MT * kTileN + (c0 + t0 + t) * kTileN + r, 0);
+#pragma unroll
+              for (int t = 0; t < 8; ++t) {
+                if (t0 + t < kCols) {
+                  float acc = 0.0f;
+#pragma unroll
+                  for (int jj = 0; jj < kMaxC; ++jj)
+                    if (jj < nc) acc += part[jj][t];
+                  facc[t0 + t] = acc;
+                }
+              }
             }
           }
         }
       }
+      if (ew == 0 && lane == 0) ISB_TRACE_CTA(23);
       if (finalize) {
         const int64_t n = static_cast<int64_t>(nt) * kTileN + r;
         if (n < p.N) {
@@ -330,12 +468,15 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
           }
         }
       }
+      if (ew == 0 && lane == 0) ISB_TRACE_CTA(17);
       u += g1 - g0;
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) ISB_TRACE(6, 0);
+  if (threadIdx.x == 0 && p.trace != nullptr) p.trace[15 * 512 + blockIdx.x] = globaltimer_();
   if (warp == 2) tmem_dealloc(tmem_base, C::kTmemCols);
 }
 
@@ -373,6 +514,7 @@ template <int MT, int PATH>
 void launch_mt(const CUtensorMap& map, const Params& prm, int grid, cudaStream_t s) {
   using C = Cfg<MT>;
   auto kern = gemm_w4a8_tc<MT, PATH>;
+  static_assert(C::kSmemBytes <= 227 * 1024, "smem");
   static bool attr_set = false;  // per instantiation; benign race (idempotent)
   if (!attr_set) {
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -380,8 +522,17 @@ void launch_mt(const CUtensorMap& map, const Params& prm, int grid, cudaStream_t
                "cudaFuncSetAttribute");
     attr_set = true;
   }
-  kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(map, prm);
-  cuda_check(cudaGetLastError(), "gemm_w4a8_tc launch");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(C::kThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, kern, map, prm), "gemm_w4a8_tc launch");
   count_launch();
 }
 
@@ -404,25 +555,36 @@ int host_cta_of(int64_t u, int64_t U, int P) {
 
 }  // namespace
 
-GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms) {
+int64_t* g_trace = nullptr;
+int g_dbg = 0;
+int g_trace_cta = 0;
+
+GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path) {
   GemmPlan pl;
   pl.mt = pick_mt(m);
   pl.m_tiles = static_cast<int>((m + pl.mt - 1) / pl.mt);
   pl.tiles = static_cast<int>(w.n_tiles) * pl.m_tiles;
   pl.units = static_cast<int64_t>(pl.tiles) * w.groups;
   pl.grid = static_cast<int>(std::min<int64_t>(num_sms, pl.units));
-  pl.maxc = 1;
-  for (int t = 0; t < pl.tiles; ++t) {
-    const int first = host_cta_of(static_cast<int64_t>(t) * w.groups, pl.units, pl.grid);
-    const int last = host_cta_of(static_cast<int64_t>(t) * w.groups + w.groups - 1, pl.units,
-                                 pl.grid);
-    pl.maxc = std::max(pl.maxc, last - first + 1);
+  auto max_contrib = [&](int grid) {
+    int mc = 1;
+    for (int t = 0; t < pl.tiles; ++t) {
+      const int first = host_cta_of(static_cast<int64_t>(t) * w.groups, pl.units, grid);
+      const int last = host_cta_of(static_cast<int64_t>(t) * w.groups + w.groups - 1, pl.units,
+                                   grid);
+      mc = std::max(mc, last - first + 1);
+    }
+    return mc;
+  };
+  pl.maxc = max_contrib(pl.grid);
+  // The fp32 path reduces split tiles in fixed order from at most 8 slices.
+  while (path == ISB_PATH_FLOAT_SCALE && pl.maxc > 8 && pl.grid > 1) {
+    pl.grid = std::max(1, pl.grid * 8 / pl.maxc - 1);
+    pl.maxc = max_contrib(pl.grid);
   }
   const int64_t counters = round_up(static_cast<int64_t>(pl.tiles) * 4, 256);
-  const int64_t partials = pl.maxc > 1
-                               ? static_cast<int64_t>(pl.tiles) * pl.maxc * pl.mt * kTileN * 4
-                               : 0;
-  pl.workspace_bytes = counters + partials;
+  const int64_t slices = pl.maxc <= 1 ? 0 : (path == ISB_PATH_INTEGER_SCALE ? 1 : pl.maxc);
+  pl.workspace_bytes = counters + static_cast<int64_t>(pl.tiles) * slices * pl.mt * kTileN * 4;
   return pl;
 }
 
@@ -445,10 +607,13 @@ void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, con
   prm.kblocks = static_cast<int>(w.kblocks);
   prm.m_tiles = pl.m_tiles;
   prm.tiles = pl.tiles;
-  prm.maxc = pl.maxc;
+  prm.maxc = path == ISB_PATH_INTEGER_SCALE ? 1 : pl.maxc;  // int path: one red.add slice
   prm.out_dtype = out_dtype;
   prm.units = pl.units;
   prm.inv_amp = std::ldexp(1.0, -w.exponent);
+  prm.trace = g_trace;
+  prm.trace_cta = g_trace_cta;
+  prm.dbg = g_dbg;
   const CUtensorMap map = make_x_map(xq, m, w.k, pl.mt);
 #define ISB_DISPATCH(MTV)                                                              \
   case MTV:                                                                            \

@@ -62,7 +62,10 @@ struct GemmPlan {
   int maxc = 1;       // max CTAs contributing to one tile
   int64_t workspace_bytes = 0;
 };
-GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms);
+extern int64_t* g_trace;  // debug timeline buffer (8 x 512 int64), nullptr = off
+extern int g_trace_cta;
+extern int g_dbg;
+GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path);
 void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                     void* out, int out_dtype, void* workspace, const GemmPlan& plan,
                     cudaStream_t s);

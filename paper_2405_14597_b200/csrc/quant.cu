@@ -84,6 +84,8 @@ __global__ void __launch_bounds__(kQuantThreads)
   __shared__ float red[kQuantThreads / 32];
   const int64_t row = blockIdx.x;
   const T* xr = x + row * k;
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();  // x may be produced by the preceding grid
   float v[V][4];
   float amax = 0.0f;
   bool finite = true;
@@ -126,6 +128,8 @@ __global__ void __launch_bounds__(kQuantThreads)
   __shared__ float red[kQuantThreads / 32];
   const int64_t row = blockIdx.x;
   const T* xr = x + row * k;
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();
   float amax = 0.0f;
   bool finite = true;
   for (int64_t e = threadIdx.x; e < k; e += kQuantThreads) {
@@ -176,20 +180,29 @@ void launch_rows(const T* x, int64_t m, int64_t k, int8_t* codes, double* scales
                       (reinterpret_cast<uintptr_t>(codes) % 4 == 0);
   const int64_t per_pass = static_cast<int64_t>(kQuantThreads) * 4;
   const int64_t v = (k + per_pass - 1) / per_pass;
-  const dim3 grid(static_cast<unsigned>(m));
-  if (vec_ok && v <= 1) {
-    quantize_rows_cached<1, T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
-  } else if (vec_ok && v <= 2) {
-    quantize_rows_cached<2, T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
-  } else if (vec_ok && v <= 4) {
-    quantize_rows_cached<4, T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
-  } else if (vec_ok && v <= 8) {
-    quantize_rows_cached<8, T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
-  } else if (vec_ok && v <= 14) {
-    quantize_rows_cached<14, T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
-  } else {
-    quantize_rows_generic<T><<<grid, kQuantThreads, 0, s>>>(x, k, codes, scales, bad);
-  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(m));
+  cfg.blockDim = dim3(kQuantThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (vec_ok && v <= 1)
+    e = cudaLaunchKernelEx(&cfg, quantize_rows_cached<1, T>, x, k, codes, scales, bad);
+  else if (vec_ok && v <= 2)
+    e = cudaLaunchKernelEx(&cfg, quantize_rows_cached<2, T>, x, k, codes, scales, bad);
+  else if (vec_ok && v <= 4)
+    e = cudaLaunchKernelEx(&cfg, quantize_rows_cached<4, T>, x, k, codes, scales, bad);
+  else if (vec_ok && v <= 8)
+    e = cudaLaunchKernelEx(&cfg, quantize_rows_cached<8, T>, x, k, codes, scales, bad);
+  else if (vec_ok && v <= 14)
+    e = cudaLaunchKernelEx(&cfg, quantize_rows_cached<14, T>, x, k, codes, scales, bad);
+  else
+    e = cudaLaunchKernelEx(&cfg, quantize_rows_generic<T>, x, k, codes, scales, bad);
+  cuda_check(e, "quantize_per_token launch");
   cuda_check(cudaGetLastError(), "quantize_per_token launch");
   count_launch();
 }
