@@ -4,6 +4,7 @@
 #include <atomic>
 #include <bit>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -186,6 +187,14 @@ void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
 }  // namespace
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ISB_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
 
 }  // namespace isb
 

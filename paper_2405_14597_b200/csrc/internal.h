@@ -39,6 +39,8 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 
 void count_launch(int n = 1);
+// Programmatic dependent launch on every kernel (env ISB_NO_PDL=1 disables; A/B only).
+bool pdl_enabled();
 
 // Kernel launchers (defined in the .cu files).
 void launch_quantize_per_token(const void* x, int x_dtype, int64_t m, int64_t k, int8_t* codes,
@@ -60,6 +62,7 @@ struct GemmPlan {
   int64_t units = 0;  // tiles * groups
   int grid = 0;
   int maxc = 1;       // max CTAs contributing to one tile
+  int cluster = 1;    // split-K ways (thread-block cluster size)
   int64_t workspace_bytes = 0;
 };
 extern int64_t* g_trace;  // debug timeline buffer (8 x 512 int64), nullptr = off
