@@ -231,9 +231,9 @@ def time_steps(fn, steps, warmup, ws):
 
 
 def gemm_kernel_timing(isb, layers, xq_sa, m, path, iters=30):
-    """Average device duration of each K3 (or K4) launch, timed with CUDA events on
-    the launching stream over back-to-back launches rotating the weight replicas
-    (weights stream from HBM)."""
+    """Average device duration of each K3 (or K4) launch: `iters` back-to-back launches
+    rotating the weight replicas (weights stream from HBM), captured in a CUDA graph so
+    host launch overhead is excluded, timed with CUDA events on the launching stream."""
     import torch
     gemm = isb.gemm_integer_scale if path == "int" else isb.gemm_float_scale
     res = []
@@ -244,10 +244,19 @@ def gemm_kernel_timing(isb, layers, xq_sa, m, path, iters=30):
         for r in range(REPLICAS):
             gemm(q, sa, layers[r][i][3], out=out, workspace=wsp)
         torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for it in range(iters):
+                    gemm(q, sa, layers[it % REPLICAS][i][3], out=out, workspace=wsp)
+        torch.cuda.current_stream().wait_stream(s)
+        g.replay()
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for it in range(iters):
-            gemm(q, sa, layers[it % REPLICAS][i][3], out=out, workspace=wsp)
+        g.replay()
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1000.0 / iters

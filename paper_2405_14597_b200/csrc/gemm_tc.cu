@@ -75,7 +75,8 @@ struct Cfg {
   // MT = 128 (prefill) finalises straight from the epilogue's registers.
   static constexpr int kPbufs = MT <= 32 ? 2 : (MT == 64 ? 1 : 0);
   static constexpr int kPbufBytes = kPbufs * MT * kTileN * 4;
-  static constexpr int kFixed = 1024 + kPbufBytes + 1024;
+  static constexpr int kSaBytes = 2 * MT * 8;  // token scales, prefetched a tile ahead
+  static constexpr int kFixed = 1024 + kPbufBytes + kSaBytes + 1024;
   static constexpr int kStagesRaw = (227 * 1024 - kFixed) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kSmemBytes = kFixed + kStages * kStageBytes;
@@ -133,8 +134,8 @@ __device__ __forceinline__ float finish(int32_t iacc, float facc, double s_a, do
 // loads (DSMEM when CC > 1) and token scales of a chunk are issued before first
 // use so the chunk costs one round trip, not one per element.
 template <int MT, int CC, int PATH>
-__device__ __forceinline__ void reduce_tile(const Params& p, uint32_t pb, int rank, int nt, int mt,
-                                            uint32_t u) {
+__device__ __forceinline__ void reduce_tile(const Params& p, uint32_t pb, const double* sa_t,
+                                            int rank, int nt, int mt, uint32_t u) {
   constexpr int SL = MT / CC;
   constexpr int CH = SL < 8 ? SL : 8;
   const int lo = rank * SL;
@@ -142,10 +143,7 @@ __device__ __forceinline__ void reduce_tile(const Params& p, uint32_t pb, int ra
   for (int c0 = 0; c0 < SL; c0 += CH) {
     double sav[CH];
 #pragma unroll
-    for (int i = 0; i < CH; ++i) {
-      const int64_t m = static_cast<int64_t>(mt) * MT + lo + c0 + i;
-      sav[i] = m < p.M ? __ldg(p.sa + m) : 0.0;
-    }
+    for (int i = 0; i < CH; ++i) sav[i] = sa_t[lo + c0 + i];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t rr = u + h * 64;
@@ -206,7 +204,8 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
   uint8_t* smem_x = smem + kStages * S * kBlockBytes;            // [stage][S][kXSlot]
   uint8_t* smem_sc = smem_x + kStages * S * kXSlot;              // [stage][S][128] scales
   uint8_t* pbuf = smem_sc + kStages * Cf::kScBytes;              // [kPbufs][MT][128] partials
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + Cf::kPbufBytes);
+  double* sa_s = reinterpret_cast<double*>(pbuf + Cf::kPbufBytes);  // [2][MT]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + Cf::kPbufBytes + Cf::kSaBytes);
   uint64_t* full = bars;
   uint64_t* empty = full + kStages;
   uint64_t* a_full = empty + kStages;
@@ -500,11 +499,29 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
       pdl_wait();  // sa and the output
       const uint32_t u = (warp - 2) * 32 + lane;  // rows u and u + 64
       const uint32_t pbuf_local = smem_u32(pbuf);
+      // Token scales of tile `it` land in sa_s[it & 1] via cp.async issued one tile
+      // ahead, so the finalise never waits on an L2/HBM round trip.
+      auto sa_prefetch = [&](int it) {
+        if (it < wk.ntiles && u < static_cast<uint32_t>(MT)) {
+          const int64_t m = static_cast<int64_t>(wk.tile(it, p) % p.m_tiles) * MT + u;
+          const uint32_t dst = smem_u32(sa_s + (it & 1) * MT + u);
+          const double* src = p.sa + (m < p.M ? m : 0);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+                       "r"(m < p.M ? 8 : 0)
+                       : "memory");
+        }
+        cp_async_commit();
+      };
+      sa_prefetch(0);
       for (int it = 0; it < wk.ntiles; ++it) {
         const int buf = it % Cf::kPbufs;
         const uint32_t ph = (it / Cf::kPbufs) & 1;
         const int tile = wk.tile(it, p);
         const int nt = tile / p.m_tiles, mt = tile % p.m_tiles;
+        sa_prefetch(it + 1);
+        cp_async_wait<1>();
+        named_bar_sync(2, 64);  // sa_s[it & 1] visible to both reduction warps
+        const double* sa_t = sa_s + (it & 1) * MT;
         mbar_wait(&pb_full[buf], ph);
         if (p.C > 1) {
           if (lane < static_cast<uint32_t>(p.C))
@@ -514,12 +531,12 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
         if (warp == 2 && lane == 0) ISB_TRACE(6, it);
         const uint32_t pb = pbuf_local + buf * (MT * kTileN * 4);
         switch (p.C) {
-          case 1: reduce_tile<MT, 1, PATH>(p, pb, wk.rank, nt, mt, u); break;
-          case 2: reduce_tile<MT, 2, PATH>(p, pb, wk.rank, nt, mt, u); break;
-          case 4: reduce_tile<MT, 4, PATH>(p, pb, wk.rank, nt, mt, u); break;
-          default: reduce_tile<MT, 8, PATH>(p, pb, wk.rank, nt, mt, u); break;
+          case 1: reduce_tile<MT, 1, PATH>(p, pb, sa_t, wk.rank, nt, mt, u); break;
+          case 2: reduce_tile<MT, 2, PATH>(p, pb, sa_t, wk.rank, nt, mt, u); break;
+          case 4: reduce_tile<MT, 4, PATH>(p, pb, sa_t, wk.rank, nt, mt, u); break;
+          default: reduce_tile<MT, 8, PATH>(p, pb, sa_t, wk.rank, nt, mt, u); break;
         }
-        __syncwarp();
+        named_bar_sync(2, 64);  // done with sa_s[it & 1] before it is refilled
         if (warp == 2 && lane == 0) ISB_TRACE(7, it);
         if (p.C > 1) {
           if (lane < static_cast<uint32_t>(p.C))
@@ -534,8 +551,10 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
     }
   }
 
+  // Peers never touch this CTA's smem after its red_empty completes (waited above),
+  // so a CTA-local barrier suffices before releasing TMEM.
   tc_fence_before();
-  if (p.C > 1) cluster_sync_all(); else __syncthreads();
+  __syncthreads();
   if (threadIdx.x == 0) ISB_TRACE_CTA(15);
   if (warp == 2) tmem_dealloc(tmem_base, Cf::kTmemCols);
 }
