@@ -10,6 +10,9 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "layout.cuh"
+
+#include <algorithm>
 
 namespace isb {
 namespace {
@@ -120,6 +123,70 @@ __global__ void __launch_bounds__(kQuantThreads)
   }
 }
 
+// Decode-sized M: a cluster of CPR CTAs shares one token row (each CTA owns a
+// contiguous K slice held in registers); the row max is combined over DSMEM, so a
+// 16-token activation is quantised by 16*CPR CTAs instead of 16.
+template <int V, typename T>
+__global__ void __launch_bounds__(kQuantThreads)
+    quantize_rows_cluster(const T* __restrict__ x, int64_t k, int64_t chunk,
+                          int8_t* __restrict__ codes, double* __restrict__ scales,
+                          int* __restrict__ bad) {
+  __shared__ float red[kQuantThreads / 32];
+  __shared__ float cta_max;
+  const uint32_t cpr = gridDim.y;                      // cluster spans blockIdx.y
+  const uint32_t rank = cluster_ctarank();
+  const int64_t row = blockIdx.x;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.y) * chunk;
+  const int64_t k1 = min(k, k0 + chunk);
+  const T* xr = x + row * k;
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();
+  float v[V][4];
+  float amax = 0.0f;
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int64_t e = k0 + (static_cast<int64_t>(i) * kQuantThreads + threadIdx.x) * 4;
+    if (e < k1) {
+      load4<T>(xr + e, v[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        finite = finite && isfinite(v[i][j]);
+        amax = fmaxf(amax, fabsf(v[i][j]));
+      }
+    }
+  }
+  if (!finite) atomicExch(bad, 1);
+  amax = block_max(amax, red);
+  if (threadIdx.x == 0) cta_max = amax;
+  cluster_sync_all();
+  if (threadIdx.x < 32) {
+    float mx = 0.0f;
+    for (uint32_t q = threadIdx.x; q < cpr; q += 32)
+      mx = fmaxf(mx, __uint_as_float(ld_shared_cluster_u32(mapa_shared(smem_u32(&cta_max), q))));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (threadIdx.x == 0) red[0] = mx;
+  }
+  cluster_sync_all();  // peers finished reading cta_max; red[0] visible CTA-wide
+  amax = red[0];
+  const double s = amax == 0.0f ? 1.0 : static_cast<double>(amax) / 127.0;
+  const double r = 1.0 / s;
+  if (threadIdx.x == 0 && rank == 0) scales[row] = s;
+  int8_t* cr = codes + row * k;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int64_t e = k0 + (static_cast<int64_t>(i) * kQuantThreads + threadIdx.x) * 4;
+    if (e < k1) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        packed |= (static_cast<uint32_t>(quant_one(v[i][j], s, r, -128, 127)) & 0xFFu) << (8 * j);
+      *reinterpret_cast<uint32_t*>(cr + e) = packed;
+    }
+  }
+}
+
 // Any K / alignment: two passes over the row (the second hits L2).
 template <typename T>
 __global__ void __launch_bounds__(kQuantThreads)
@@ -190,6 +257,29 @@ void launch_rows(const T* x, int64_t m, int64_t k, int8_t* codes, double* scales
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e;
+  // Decode-sized M: spread each row over a cluster of CTAs (<= 1024 elements each).
+  const int64_t cpr = std::min<int64_t>(8, (k + 1023) / 1024);
+  if (vec_ok && m < 148 && cpr > 1 && round_up((k + cpr - 1) / cpr, 4) <= 4096) {
+    const int64_t chunk = round_up((k + cpr - 1) / cpr, 4);
+    cfg.gridDim = dim3(static_cast<unsigned>(m), static_cast<unsigned>(cpr));
+    cudaLaunchAttribute cattr[2];
+    cattr[0] = attr[0];
+    cattr[1].id = cudaLaunchAttributeClusterDimension;
+    cattr[1].val.clusterDim.x = 1;
+    cattr[1].val.clusterDim.y = static_cast<unsigned>(cpr);
+    cattr[1].val.clusterDim.z = 1;
+    cfg.attrs = cattr;
+    cfg.numAttrs = 2;
+    if (chunk <= 1024)
+      e = cudaLaunchKernelEx(&cfg, quantize_rows_cluster<1, T>, x, k, chunk, codes, scales, bad);
+    else if (chunk <= 2048)
+      e = cudaLaunchKernelEx(&cfg, quantize_rows_cluster<2, T>, x, k, chunk, codes, scales, bad);
+    else
+      e = cudaLaunchKernelEx(&cfg, quantize_rows_cluster<4, T>, x, k, chunk, codes, scales, bad);
+    cuda_check(e, "quantize_per_token launch");
+    count_launch();
+    return;
+  }
   if (vec_ok && v <= 1)
     e = cudaLaunchKernelEx(&cfg, quantize_rows_cached<1, T>, x, k, codes, scales, bad);
   else if (vec_ok && v <= 2)
