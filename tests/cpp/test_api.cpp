@@ -1,0 +1,315 @@
+// C++ drop-in tests: the reference's own hot-path test cases (proj/tests/*.cpp)
+// run against the B200 library through the reference-signature C++ API
+// (include/intscale/*.hpp). Cases cite the reference test they mirror. Needs a GPU.
+#include <intscale/analysis.hpp>
+#include <intscale/gemm.hpp>
+#include <intscale/integer_scale.hpp>
+#include <intscale/quantize.hpp>
+#include <intscale/tensor_io.hpp>
+
+#include <bit>
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+using namespace intscale;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(c)                                                              \
+  do {                                                                        \
+    ++g_checks;                                                               \
+    if (!(c)) {                                                               \
+      ++g_fail;                                                               \
+      std::printf("  CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);       \
+    }                                                                         \
+  } while (0)
+#define CHECK_THROWS_AS(expr, T)                                              \
+  do {                                                                        \
+    ++g_checks;                                                               \
+    bool ok = false;                                                          \
+    try {                                                                     \
+      (void)(expr);                                                           \
+    } catch (const T&) {                                                      \
+      ok = true;                                                              \
+    } catch (...) {                                                           \
+    }                                                                         \
+    if (!ok) {                                                                \
+      ++g_fail;                                                               \
+      std::printf("  CHECK_THROWS_AS failed %s:%d: %s\n", __FILE__, __LINE__, #expr); \
+    }                                                                         \
+  } while (0)
+
+static std::int64_t ulp_distance(float a, float b) {  // test_gemm.cpp:22-29
+  if (a == b) return 0;
+  auto key = [](float x) {
+    auto u = std::bit_cast<std::int32_t>(x);
+    return std::int64_t{u < 0 ? std::numeric_limits<std::int32_t>::min() - std::int64_t{u} : u};
+  };
+  return std::abs(key(a) - key(b));
+}
+
+static QuantizedTensor make_activation(std::initializer_list<std::initializer_list<int>> rows,
+                                       std::initializer_list<double> scales) {
+  QuantizedTensor t;
+  t.values.resize(static_cast<Index>(rows.size()), static_cast<Index>(rows.begin()->size()));
+  Index i = 0;
+  for (auto& r : rows) {
+    Index j = 0;
+    for (int v : r) t.values(i, j++) = static_cast<std::int16_t>(v);
+    ++i;
+  }
+  t.params.bit_width = 8;
+  t.params.scheme = Scheme::symmetric;
+  t.params.granularity = Granularity::per_token();
+  t.params.scales.resize(static_cast<Index>(scales.size()));
+  Index u = 0;
+  for (double s : scales) t.params.scales[u++] = s;
+  return t;
+}
+
+static QuantizedTensor make_weight(std::initializer_list<std::initializer_list<int>> rows,
+                                   std::initializer_list<double> scales, int bits, Granularity g) {
+  QuantizedTensor t = make_activation(rows, scales);
+  t.params.bit_width = bits;
+  t.params.granularity = g;
+  return t;
+}
+
+static void test_scalar_hand_example() {  // test_gemm.cpp:94-118
+  auto x = make_activation({{2, 3}}, {0.5});
+  auto w = make_weight({{4}, {5}}, {0.25, 0.125}, 4, Granularity::group_of(1));
+  auto rf = gemm_float_scale(x, w);
+  CHECK(rf.output(0, 0) == 1.9375f);
+  CHECK(rf.stats.int_to_float_conversions == 2);
+  CHECK(rf.stats.integer_multiply_adds == 2);
+  CHECK(rf.stats.max_abs_accumulator == 15);
+  CHECK(!rf.stats.overflow_detected);
+  auto set = integerize_scales(w.params.scales, 8);
+  CHECK(set.int_scales[0] == 2);
+  CHECK(set.int_scales[1] == 1);
+  auto ri = gemm_integer_scale(x, w, set);
+  CHECK(ri.output(0, 0) == 1.9375f);
+  CHECK(ri.stats.int_to_float_conversions == 1);
+  CHECK(ri.stats.integer_multiply_adds == 4);
+  CHECK(ri.stats.max_abs_accumulator == 31);
+}
+
+static void test_unit_scales() {  // test_gemm.cpp:120-135
+  auto x = make_activation({{1, 2, 3, 4}, {-1, 0, 1, 0}}, {1.0, 1.0});
+  auto w = make_weight({{1, -1}, {2, 0}, {0, 3}, {-2, 1}}, {1.0, 1.0}, 4, Granularity::per_channel());
+  auto rf = gemm_float_scale(x, w);
+  CHECK(rf.output(0, 0) == -3.0f);
+  CHECK(rf.output(0, 1) == 12.0f);
+  CHECK(rf.output(1, 0) == -1.0f);
+  CHECK(rf.output(1, 1) == 4.0f);
+}
+
+static void test_validation() {  // test_gemm.cpp:303-339
+  auto x = make_activation({{1, 2}}, {1.0});
+  auto w = make_weight({{1}, {1}}, {1.0}, 4, Granularity::group_of(1));
+  CHECK_THROWS_AS(gemm_float_scale(x, w), ParamError);
+  auto w3 = make_weight({{1}, {1}, {1}}, {1.0, 1.0, 1.0}, 4, Granularity::group_of(1));
+  CHECK_THROWS_AS(gemm_float_scale(x, w3), DimensionError);
+  auto wok = make_weight({{1}, {1}}, {1.0, 1.0}, 4, Granularity::group_of(1));
+  auto xs = x;
+  xs.params.granularity = Granularity::per_tensor();
+  CHECK_THROWS_AS(gemm_float_scale(xs, wok), ParamError);
+  auto x4 = x;
+  x4.params.bit_width = 4;
+  CHECK_THROWS_AS(gemm_float_scale(x4, wok), ParamError);
+  auto xneg = make_activation({{-128, 0}}, {1.0});
+  CHECK_THROWS_AS(gemm_float_scale(xneg, wok), ValueError);
+  auto wbig = make_weight({{9}, {1}}, {1.0, 1.0}, 4, Granularity::group_of(1));
+  CHECK_THROWS_AS(gemm_float_scale(x, wbig), ValueError);
+  auto set = integerize_scales(wok.params.scales, 8);
+  auto tampered = set;
+  tampered.int_scales[0] += 1;
+  CHECK_THROWS_AS(gemm_integer_scale(x, wok, tampered), ParamError);
+}
+
+static void test_overflow_rig() {  // test_gemm.cpp:345-407
+  MatF xf = MatF::Constant(1, 4096, 127.0f);
+  auto x = quantize(xf, 8, Scheme::symmetric, Granularity::per_token());
+  MatF wf = MatF::Constant(4096, 2, -8.0f);
+  auto w = quantize(wf, 4, Scheme::symmetric, Granularity::group_of(128));
+  auto set = integerize_scales(w.params.scales, 1024);
+  CHECK(x.params.scales[0] == 1.0);
+  CHECK(w.values.minCoeff() == -7 && w.values.maxCoeff() == -7);
+  CHECK(set.int_scales.minCoeff() == 1170 && set.int_scales.maxCoeff() == 1170);
+  auto r = gemm_integer_scale(x, w, set);
+  CHECK(r.stats.overflow_detected);
+  CHECK(r.stats.max_abs_accumulator == std::int64_t{113792} * 1170 * 32);
+  auto report = overflow_analyzer(4096, 128, 8, 4, set);
+  CHECK(!report.safe);
+  GemmOptions strict;
+  strict.overflow = OverflowMode::strict;
+  bool threw = false;
+  try {
+    gemm_integer_scale(x, w, set, strict);
+  } catch (const OverflowError& e) {
+    threw = std::string(e.what()).find("(0, 0)") != std::string::npos;
+  }
+  CHECK(threw);
+  PathConfig path{PathKind::integer_scale, &set, nullptr};
+  auto fb = run_layer(x, w, path, FallbackPolicy::float_scale_on_overflow_risk);
+  CHECK(fb.stats.fallback_applied);
+  auto rf = gemm_float_scale(x, w);
+  CHECK(fb.output == rf.output);
+  CHECK(fb.stats.int_to_float_conversions == 2 * 32);
+  auto rn = run_layer(x, w, path, FallbackPolicy::none);
+  CHECK(!rn.stats.fallback_applied && rn.stats.overflow_detected);
+}
+
+static void test_quantizer_pins() {  // test_quantize.cpp:92-97, :330-339
+  MatF one(1, 1);
+  one(0, 0) = 1.0f;
+  auto q8 = quantize(one, 8, Scheme::symmetric, Granularity::per_token());
+  CHECK(q8.params.scales[0] == 1.0 / 127.0);
+  CHECK(q8.values(0, 0) == 127);
+  MatF x(3, 2);
+  x(0, 0) = 1.0f; x(0, 1) = -2.0f; x(1, 0) = 0.5f; x(1, 1) = 0.25f; x(2, 0) = 0.0f; x(2, 1) = 0.0f;
+  auto q = quantize(x, 8, Scheme::symmetric, Granularity::per_token());
+  CHECK(q.params.scales[0] == 2.0 / 127.0);
+  CHECK(q.params.scales[1] == 0.5 / 127.0);
+  CHECK(q.params.scales[2] == 1.0);
+  CHECK(q.values(0, 1) == -127);
+  MatF w1(2, 2);  // test_integer_scale.cpp:127-132 (ties away: -3.5 -> -4)
+  w1(0, 0) = 0.875f; w1(0, 1) = 3.5f; w1(1, 0) = -0.4375f; w1(1, 1) = -1.75f;
+  auto qw = quantize(w1, 4, Scheme::symmetric, Granularity::group_of(2));
+  CHECK(qw.params.scales[0] == 0.125 && qw.params.scales[1] == 0.5);
+  CHECK(qw.values(0, 0) == 7 && qw.values(1, 0) == -4 && qw.values(0, 1) == 7 && qw.values(1, 1) == -4);
+}
+
+static void test_integer_scale_pins() {  // test_integer_scale.cpp:26-66
+  CHECK(search_amplifier(VecD{0.3, 0.9, 5.0}) == 4);
+  CHECK(search_amplifier(VecD{0.5}) == 2);
+  CHECK(search_amplifier(VecD{1.5, 2.0}) == 1);
+  CHECK(search_amplifier(VecD{0x1.0p-10}) == 1024);
+  CHECK(search_amplifier_exponent(VecD{0x1.0p-10, 0.25}) == 10);
+  CHECK_THROWS_AS(search_amplifier(VecD{}), ParamError);
+  CHECK_THROWS_AS(search_amplifier(VecD{1e-300}), ParamError);
+  auto s = integerize_scales(VecD{0.25, 0.125}, 8);
+  CHECK(s.amplifier == 8 && s.exponent == 3 && s.int_scales[0] == 2 && s.int_scales[1] == 1);
+  CHECK(integerize_scales(VecD{0.0001}, 1024).int_scales[0] == 1);
+  CHECK(integerize_scales(VecD{2.5 / 1024}, 1024).int_scales[0] == 3);
+  CHECK_THROWS_AS(integerize_scales(VecD{0.5}, 3), ParamError);
+  CHECK_THROWS_AS(integerize_scales(VecD{3.0e6}, 1024), OverflowError);
+}
+
+static void test_nibble_pins() {  // test_tensor_io.cpp:65-86
+  MatQ v(1, 2);
+  v(0, 0) = -8; v(0, 1) = 7;
+  auto p = pack_signed4(v);
+  CHECK(p.size() == 1 && p[0] == 0x78);
+  CHECK(unpack_signed4(p, 1, 2) == v);
+  MatQ v8(1, 8);
+  const int vals[8] = {-8, -1, 0, 1, 2, -2, 7, -7};
+  for (int i = 0; i < 8; ++i) v8(0, i) = static_cast<std::int16_t>(vals[i]);
+  CHECK((pack_signed4(v8) == std::vector<std::uint8_t>{0xf8, 0x10, 0xe2, 0x97}));
+  CHECK(unpack_signed4({0xf8, 0x10, 0xe2, 0x97}, 1, 8) == v8);
+  MatQ bad(1, 1);
+  bad(0, 0) = 8;
+  CHECK_THROWS_AS(pack_signed4(bad), ValueError);
+  CHECK_THROWS_AS(unpack_signed4({0xf8}, 1, 3), LengthError);
+}
+
+static void test_overflow_bound_pins() {  // test_analysis.cpp:33-62
+  IntegerScaleSet one;
+  one.int_scales = VecI{1};
+  CHECK(overflow_analyzer(128, 128, 8, 4, one).static_bound == 130048);
+  IntegerScaleSet s;
+  s.int_scales = VecI::Constant(32, 1024);
+  s.amplifier = 1024;
+  s.exponent = 10;
+  auto r = overflow_analyzer(4096, 128, 8, 4, s);
+  CHECK(r.static_bound == 4261412864LL && !r.safe);
+  IntegerScaleSet f;
+  f.int_scales = VecI{1, 2, 3, 4};
+  CHECK(overflow_analyzer(4, 2, 4, 4, f).static_bound == 784);
+}
+
+// acceptance.cpp:86-128 (criterion 1): dyadic scales => integer and float paths agree.
+static void test_dyadic_agreement() {
+  std::mt19937_64 rng(1001);
+  auto below = [&](std::int64_t n) { return static_cast<std::int64_t>(rng() % n); };
+  std::int64_t worst = 0;
+  for (int trial = 0; trial < 40; ++trial) {
+    const Index m = 1 + below(16), n = 1 + below(40), k = 4 * (1 + below(16));
+    const Index g_choices[] = {1, 2, 4, k};
+    const Index g = g_choices[below(4)];
+    const Index units = (k / g) * n;
+    VecD ws(units), xs(m);
+    for (Index u = 0; u < units; ++u) ws[u] = double(1 + below(4096)) / 1024.0;
+    for (Index i = 0; i < m; ++i) xs[i] = double(1 + below(1024)) / 256.0;
+    QuantizedTensor x, w;
+    x.values.resize(m, k);
+    for (Index i = 0; i < m * k; ++i) x.values.data()[i] = static_cast<std::int16_t>(below(255) - 127);
+    x.params = {8, Scheme::symmetric, Granularity::per_token(), xs, VecI()};
+    w.values.resize(k, n);
+    for (Index i = 0; i < k * n; ++i) w.values.data()[i] = static_cast<std::int16_t>(below(16) - 8);
+    w.params = {4, Scheme::symmetric, Granularity::group_of(g), ws, VecI()};
+    auto set = integerize_scales(ws, 1024);
+    auto rf = gemm_float_scale(x, w);
+    auto ri = gemm_integer_scale(x, w, set);
+    for (Index i = 0; i < m * n; ++i)
+      worst = std::max(worst, ulp_distance(rf.output.data()[i], ri.output.data()[i]));
+  }
+  CHECK(worst <= 1);
+}
+
+// A LLaMA-shaped layer goes through tcgen05 and matches the exact int64 pass.
+static void test_tensor_core_layer() {
+  std::mt19937_64 rng(42);
+  auto u01 = [&] { return (rng() >> 11) * 0x1.0p-53; };
+  const Index m = 16, k = 1024, n = 384;
+  MatF wf(k, n), xf(m, k);
+  for (Index c = 0; c < n; ++c)
+    for (Index t = 0; t < k / 128; ++t) {
+      const double vmax = 7.0 * std::exp2(-9.99 + 3.94 * u01());
+      for (Index r = t * 128; r < (t + 1) * 128; ++r)
+        wf(r, c) = static_cast<float>((2.0 * u01() - 1.0) * 0.97 * vmax);
+      wf(t * 128, c) = static_cast<float>(vmax);
+    }
+  for (Index i = 0; i < m * k; ++i) xf.data()[i] = static_cast<float>(4.0 * u01() - 2.0);
+  auto w = quantize(wf, 4, Scheme::symmetric, Granularity::group_of(128));
+  auto x = quantize(xf, 8, Scheme::symmetric, Granularity::per_token());
+  auto set = integerize_scales(w.params.scales, search_amplifier(w.params.scales));
+  auto r = gemm_integer_scale(x, w, set);  // throws if tcgen05 and int64 outputs differ
+  CHECK(r.stats.tensor_core);
+  CHECK(r.stats.max_abs_accumulator > 0);
+  GemmOptions fast;
+  fast.track_accumulator = false;
+  auto r2 = gemm_integer_scale(x, w, set, fast);
+  CHECK(r2.output == r.output);
+  CHECK(r2.stats.max_abs_accumulator == -1);
+}
+
+int main() {
+  const std::pair<const char*, std::function<void()>> tests[] = {
+      {"scalar_hand_example", test_scalar_hand_example},
+      {"unit_scales", test_unit_scales},
+      {"validation", test_validation},
+      {"overflow_rig", test_overflow_rig},
+      {"quantizer_pins", test_quantizer_pins},
+      {"integer_scale_pins", test_integer_scale_pins},
+      {"nibble_pins", test_nibble_pins},
+      {"overflow_bound_pins", test_overflow_bound_pins},
+      {"dyadic_agreement", test_dyadic_agreement},
+      {"tensor_core_layer", test_tensor_core_layer},
+  };
+  for (const auto& [name, fn] : tests) {
+    const int before = g_fail;
+    try {
+      fn();
+    } catch (const std::exception& e) {
+      ++g_fail;
+      std::printf("  exception: %s\n", e.what());
+    }
+    std::printf("%s %s\n", g_fail == before ? "PASS" : "FAIL", name);
+  }
+  std::printf("%d checks, %d failed\n", g_checks, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}
