@@ -134,6 +134,17 @@ isb_weight* pack_common(const int16_t* codes, const uint8_t* s4, int64_t k, int6
         mx = std::max(mx, v);
       }
       w->max_int_scale = mx;
+      // static bound max_col sum_g g*127*8*k_g (A_max 127, W_max 8), saturated
+      int64_t worst = 0;
+      for (int64_t c = 0; c < n; ++c) {
+        int64_t col = 0;
+        for (int64_t g = 0; g < w->groups; ++g) {
+          col += group * 127 * 8 * static_cast<int64_t>(h[static_cast<size_t>(c * w->groups + g)]);
+          if (col > (int64_t{1} << 62)) break;
+        }
+        worst = std::max(worst, col);
+      }
+      w->static_bound = worst;
     }
     DeviceFlag bad(s);
     launch_pack(codes, s4, k, n, w->packed, w->kblocks, w->n_tiles, bad.d, s);

@@ -55,7 +55,7 @@ template <int MT>
 struct Cfg {
   static constexpr int S = MT <= 32 ? 4 : (MT == 64 ? 2 : 1);    // 128-K blocks per step
   static constexpr int kXformWG = MT >= 128 ? 1 : 2;             // transform warpgroups
-  static constexpr int kEpiWG = MT >= 128 ? 2 : 1;               // epilogue warpgroups
+  static constexpr int kEpiWG = MT >= 128 ? 4 : 1;               // epilogue warpgroups
   static constexpr int kCols = MT / kEpiWG;                      // tokens per epilogue thread
   static constexpr int kThreads = 128 + 128 * kXformWG + 128 * kEpiWG;
   static constexpr int kNA = MT <= 32 ? 2 : (MT == 64 ? 3 : 4);  // TMEM A stages (S*32 cols)
@@ -93,6 +93,7 @@ struct Params {
   int M, N, G, gb, kblocks, m_tiles, tiles, out_dtype;
   int C, NC;              // cluster size, number of clusters
   double inv_amp;         // 2^-e (exact)
+  int late_shift;         // 16 * static bound fits int32: accumulate 16*P*k, shift once
   int64_t* trace;         // optional debug timeline (see ISB_TRACE)
   int trace_cta;
   int dbg;                // debug knobs: 1 skip A st, 2 skip D ld, 4 skip MMA issue
@@ -390,10 +391,23 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
     const int c0 = wg * kCols;
     pdl_wait();  // sa and the output may be touched by the preceding grid
     const uint32_t pbuf_local = smem_u32(pbuf);
+    const bool late = p.late_shift != 0;
     int j = 0;   // global step index
     for (int it = 0; it < wk.ntiles; ++it) {
       const int tile = wk.tile(it, p);
       const int nt = tile / p.m_tiles, mt = tile % p.m_tiles;
+      if constexpr (Cf::kPbufs == 0) {
+        if (ew == 0) {  // token scales of this tile -> sa_s[it & 1] (read at finalise)
+          for (int t = lane; t < MT; t += 32) {
+            const int64_t m = static_cast<int64_t>(mt) * MT + t;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                             smem_u32(sa_s + (it & 1) * MT + t)),
+                         "l"(p.sa + (m < p.M ? m : 0)), "r"(m < p.M ? 8 : 0)
+                         : "memory");
+          }
+          cp_async_commit();
+        }
+      }
       int32_t iacc[kCols];
       float facc[kCols];
       int32_t gsum[GB1 ? 1 : kCols];
@@ -446,10 +460,15 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
                   gsum[cc + t] = d;
                 }
                 if (g_last) {
-                  if (PATH == ISB_PATH_INTEGER_SCALE)
-                    iacc[cc + t] += (d >> 4) * kg;  // Eq. 2: int32 scaled accumulation
-                  else
+                  if (PATH == ISB_PATH_INTEGER_SCALE) {
+                    // Eq. 2: int32 scaled accumulation. With 16x headroom under the
+                    // static bound the x16 of the nibble expansion is removed once at
+                    // the end (one IMAD per value instead of SHF + IMAD).
+                    if (late) iacc[cc + t] += d * kg;
+                    else iacc[cc + t] += (d >> 4) * kg;
+                  } else {
                     facc[cc + t] = fmaf(static_cast<float>(d), sg, facc[cc + t]);  // Eq. 1, fp32
+                  }
                 }
               }
             }
@@ -461,6 +480,10 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
           mbar_arrive(&d_empty[ds]);
           mbar_arrive(&sc_empty[stage]);
         }
+      }
+      if (PATH == ISB_PATH_INTEGER_SCALE && late) {
+#pragma unroll
+        for (int t = 0; t < kCols; ++t) iacc[t] >>= 4;  // exact: 16 | acc16
       }
       // ------------------------------------------------ tile completion
       if (ew == 0 && lane == 0) ISB_TRACE(8, it);
@@ -478,6 +501,11 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&pb_full[buf]);
       } else {
+        // Direct finalise from registers (MT = 128): token scales were prefetched
+        // into sa_s at the start of the tile.
+        if (ew == 0) cp_async_wait<0>();
+        named_bar_sync(1, 128 * Cf::kEpiWG);
+        const double* sa_t = sa_s + (it & 1) * MT;
         const int64_t n = static_cast<int64_t>(nt) * kTileN + r;
         if (n < p.N) {
 #pragma unroll
@@ -485,7 +513,7 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
             const int64_t m = static_cast<int64_t>(mt) * MT + c0 + t;
             if (m < p.M)
               store_out(p.out, p.out_dtype, m * p.N + n,
-                        finish<PATH>(iacc[t], facc[t], __ldg(p.sa + m), p.inv_amp));
+                        finish<PATH>(iacc[t], facc[t], sa_t[c0 + t], p.inv_amp));
           }
         }
       }
@@ -737,6 +765,8 @@ void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, con
   prm.trace = g_trace;
   prm.trace_cta = g_trace_cta;
   prm.dbg = g_dbg;
+  prm.late_shift = (path == ISB_PATH_INTEGER_SCALE && w.static_bound > 0 &&
+                    w.static_bound <= (int64_t{1} << 27) - 1) ? 1 : 0;
   const CUtensorMap map = make_x_map(xq, m, w.k, pl.mt);
   const bool gb1 = prm.gb == 1;
 #define ISB_DISPATCH(MTV)                                                                   \

@@ -14,6 +14,7 @@ struct isb_weight {
   int32_t exponent = 0;
   int32_t has_int_scales = 0;
   int32_t max_int_scale = 0;
+  int64_t static_bound = 0;  // overflow_analyzer bound of the int scales (analysis.cpp:24-59)
   int64_t kblocks = 0;   // ceil(K / 128)
   int64_t n_tiles = 0;   // ceil(N / 128)
   uint8_t* packed = nullptr;        // n_tiles * kblocks * 8 KiB
