@@ -167,6 +167,15 @@ isb_weight* pack_common(const int16_t* codes, const uint8_t* s4, int64_t k, int6
   return w;
 }
 
+// ISB_NO_FOLD=1 forces the per-group kernel at prefill sizes (A/B measurements).
+bool fold_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("ISB_NO_FOLD");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
 void require_gemm_args(const int8_t* xq, const double* sa, int64_t m, int64_t k,
                        const isb_weight* w, int out_dtype) {
   if (!w) fail(ISB_PARAM, "null weight handle");
@@ -192,6 +201,10 @@ void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
   const GemmPlan pl = plan_gemm(m, *w, num_sms(), path);
   if (!ws || ws_bytes < pl.workspace_bytes)
     fail(ISB_PARAM, "workspace too small: need " + std::to_string(pl.workspace_bytes) + " bytes");
+  if (fold_eligible(m, *w, path) && !fold_disabled()) {
+    launch_gemm_fold(xq, sa, m, *w, out, out_dtype, num_sms(), as_stream(stream));
+    return;
+  }
   launch_gemm_tc(path, xq, sa, m, *w, out, out_dtype, ws, pl, as_stream(stream));
 }
 

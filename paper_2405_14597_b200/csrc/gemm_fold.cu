@@ -1,0 +1,368 @@
+// K3 prefill variant — integer scale FOLDED into the weight expansion.
+//
+// Reference: gemm_integer_scale (gemm.cpp:205-262), paper Eq. 2:
+//   acc = sum_g k_g * P_g,  P_g = sum_{k in g} x_k * w_k  (int32, exact).
+// Because k_g is an integer, sum_g k_g * P_g = sum_k x_k * (k_g(k) * w_k): when
+// every k_g <= 16, k_g * w lies in [-128, 112] and fits the int8 tensor-core
+// operand, so the transform warps expand int4 -> (k_g * w) int8 and the tensor
+// core accumulates the whole K reduction — the scaled int32 accumulator — in
+// TMEM, with no per-group epilogue at all (SURVEY H1 "k <= 16 fold band";
+// llama_like weights at alpha = 1024 have k_g in [1, 15]). The result is
+// bit-identical to the per-group kernel: every partial sum is bounded by the
+// static overflow bound (analysis.cpp:24-59), which callers gate on.
+//
+// Tile: 128 output channels (UMMA M) x 192 tokens (UMMA N), persistent CTAs.
+// TMEM: A ring 4 x 32 columns (expanded weights) + 2 x 192-column int32
+// accumulators, so the epilogue of tile t overlaps the MMAs of tile t+1.
+//
+//   warp 0      producer : per 128-K block one bulk copy of the 8 KiB packed
+//                          weight block + 512 B of k_g, and a TMA (SWIZZLE_128B)
+//                          of the 192 x 128 int8 activation tile.
+//   warp 1      MMA      : 4 x tcgen05.mma.kind::i8 (K = 32) per block into D[t & 1].
+//   warp 2      TMEM allocator.
+//   warps 4-11  transform: two warpgroups alternate blocks; thread r owns channel r:
+//                          nibble -> fp16 lane (exponent-bias trick) -> one HFMA2
+//                          computes 1536 + k*c exactly -> low byte = k*c.
+//   warps 12-15 epilogue : tcgen05.ld of D, out = float((double(acc) / 2^e) * s_a).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.h"
+#include "layout.cuh"
+
+namespace isb {
+namespace {
+
+constexpr int kFMT = 192;                     // tokens per tile (UMMA N)
+constexpr int kFXBytes = kFMT * 128;          // 24 KiB activation tile per block
+constexpr int kFStage = kBlockBytes + kFXBytes;  // 32 KiB (W first, X 1024-aligned)
+constexpr int kFNA = 4;                       // TMEM A ring
+constexpr int kFXformWG = 2;
+constexpr int kFThreads = 128 + 128 * kFXformWG + 128;
+constexpr int kFStages = 6;
+constexpr int kFSmem = 1024 + kFStages * (kFStage + kTileN * 4) + 2 * kFMT * 8 + 512;
+static_assert(kFSmem <= 227 * 1024, "smem");
+constexpr uint32_t kFDCol = kFNA * 32;        // D buffers start after the A ring
+
+struct FoldParams {
+  const uint8_t* packed;  // [n_tiles][kblocks][8 KiB]
+  const int32_t* kscale;  // [n_tiles][G][128]
+  const double* sa;       // [M]
+  void* out;              // [M][N]
+  int M, N, G, gb, kblocks, m_tiles, tiles, out_dtype;
+  double inv_amp;
+};
+
+__device__ __forceinline__ void store_out_f(void* out, int dtype, int64_t idx, float f) {
+  if (dtype == ISB_F32)
+    static_cast<float*>(out)[idx] = f;
+  else if (dtype == ISB_BF16)
+    static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(f);
+  else
+    static_cast<__half*>(out)[idx] = __float2half_rn(f);
+}
+
+// ((w ^ x) & m) | o as one LOP3 (x subset of m, o disjoint from m):
+// f(w, b = m, c = x | o) = b ? (w ^ c) : c  -> LUT 0x6A.
+__device__ __forceinline__ uint32_t lop_extract(uint32_t w, uint32_t m, uint32_t xo) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x6A;" : "=r"(d) : "r"(w), "r"(m), "r"(xo));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t half2_bits(float v) {
+  const __half h = __float2half_rn(v);
+  const uint32_t u = __half_as_ushort(h);
+  return u | (u << 16);
+}
+
+// One packed word (8 two's-complement nibbles; byte b = code(k0+b) | code(k0+4+b) << 4)
+// -> k*code for k0..k0+3 (lo) and k0+4..k0+7 (hi), int8 lanes.
+// Nibble n at bit 0 of a 16-bit lane, biased (XOR 8 -> c + 8) and OR'ed into an fp16
+// with exponent field 0x64 is exactly 1024 + (c + 8); at bit 4 it is 1024 + 16 (c + 8).
+// HFMA2 (exact: the result is an integer in [1408, 1648], representable) gives
+// 1536 + k*c, whose low mantissa byte is (512 + k*c) mod 256 = k*c mod 256.
+__device__ __forceinline__ void fold_word(uint32_t w, uint32_t k1, uint32_t k16, uint32_t cA,
+                                          uint32_t cB, uint32_t& lo, uint32_t& hi) {
+  const uint32_t w8 = w >> 8;
+  const uint32_t hA = lop_extract(w, 0x000F000Fu, 0x64086408u);   // codes k0, k0+2
+  const uint32_t hB = lop_extract(w, 0x00F000F0u, 0x64806480u);   // k0+4, k0+6
+  const uint32_t hC = lop_extract(w8, 0x000F000Fu, 0x64086408u);  // k0+1, k0+3
+  const uint32_t hD = lop_extract(w8, 0x00F000F0u, 0x64806480u);  // k0+5, k0+7
+  const uint32_t rA = hfma2(hA, k1, cA);
+  const uint32_t rB = hfma2(hB, k16, cB);
+  const uint32_t rC = hfma2(hC, k1, cA);
+  const uint32_t rD = hfma2(hD, k16, cB);
+  lo = __byte_perm(rA, rC, 0x6240);
+  hi = __byte_perm(rB, rD, 0x6240);
+}
+
+__global__ void __launch_bounds__(kFThreads, 1)
+    gemm_w4a8_fold(const __grid_constant__ CUtensorMap x_map, const FoldParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smem_sc = smem + kFStages * kFStage;                        // [stage][128] k_g
+  double* sa_s = reinterpret_cast<double*>(smem_sc + kFStages * kTileN * 4);  // [2][MT]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sa_s + 2 * kFMT);
+  uint64_t* empty = full + kFStages;
+  uint64_t* a_full = empty + kFStages;
+  uint64_t* a_empty = a_full + kFNA;
+  uint64_t* d_full = a_empty + kFNA;
+  uint64_t* d_empty = d_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int ntiles = static_cast<int>(blockIdx.x) < p.tiles
+                         ? (p.tiles - static_cast<int>(blockIdx.x) + gridDim.x - 1) / gridDim.x
+                         : 0;
+  const int total = ntiles * p.kblocks;  // (tile, block) steps of this CTA
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tensormap(&x_map);
+    for (int i = 0; i < kFStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1 + 4);
+    }
+    for (int i = 0; i < kFNA; ++i) {
+      mbar_init(&a_full[i], 4);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&d_full[i], 1);
+      mbar_init(&d_empty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) pdl_launch_dependents();
+
+  auto tile_of = [&](int it, int& nt, int& mt) {
+    const int t = blockIdx.x + it * gridDim.x;
+    nt = t / p.m_tiles;
+    mt = t % p.m_tiles;
+  };
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- producer
+    if (elect_one()) {
+      auto load_static = [&](int j, int stage) {
+        int nt, mt;
+        tile_of(j / p.kblocks, nt, mt);
+        const int kb = j % p.kblocks;
+        mbar_arrive_expect_tx(&full[stage], kFStage + kTileN * 4);
+        bulk_load(smem + stage * kFStage,
+                  p.packed + (static_cast<int64_t>(nt) * p.kblocks + kb) * kBlockBytes,
+                  kBlockBytes, &full[stage]);
+        bulk_load(smem_sc + stage * kTileN * 4,
+                  p.kscale + (static_cast<int64_t>(nt) * p.G + kb / p.gb) * kTileN, kTileN * 4,
+                  &full[stage]);
+      };
+      const int pre = min(total, kFStages);
+      for (int j = 0; j < pre; ++j) load_static(j, j);
+      pdl_wait();
+      for (int j = 0; j < total; ++j) {
+        const int stage = j % kFStages;
+        if (j >= pre) {
+          mbar_wait(&empty[stage], ((j / kFStages) & 1) ^ 1);
+          load_static(j, stage);
+        }
+        int nt, mt;
+        tile_of(j / p.kblocks, nt, mt);
+        tma_load_2d(smem + stage * kFStage + kBlockBytes, &x_map, &full[stage],
+                    (j % p.kblocks) * kBlockK, mt * kFMT);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = make_idesc_i8(128, kFMT);
+    const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint32_t s_base = smem_u32(smem);
+    int j = 0;
+    for (int it = 0; it < ntiles; ++it) {
+      const int ds = it & 1;
+      mbar_wait(&d_empty[ds], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tbase + kFDCol + ds * kFMT;
+      for (int kb = 0; kb < p.kblocks; ++kb, ++j) {
+        const int stage = j % kFStages, as = j % kFNA;
+        mbar_wait(&a_full[as], (j / kFNA) & 1);  // implies full[stage] (transform saw it)
+        tc_fence_after();
+        const uint64_t bdesc = make_sw128_kmajor_desc(s_base + stage * kFStage + kBlockBytes);
+        const uint32_t a_tmem = tbase + as * 32;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          mma_i8_ts_warp(d_tmem, a_tmem + c * 8, bdesc + static_cast<uint64_t>(c * 2), idesc,
+                         (kb > 0 || c > 0) ? 1u : 0u);
+        mma_commit_warp(&empty[stage]);
+        mma_commit_warp(&a_empty[as]);
+      }
+      mma_commit_warp(&d_full[ds]);
+    }
+  } else if (warp >= 4 && warp < 4 + 4 * kFXformWG) {
+    // ---------------------------------------------------------------- transform
+    const int xw = static_cast<int>(warp - 4) / 4;
+    const uint32_t r = (warp % 4) * 32 + lane;  // output channel == TMEM lane
+    const uint32_t lane_base = ((warp % 4) * 32) << 16;
+    const uint32_t w_base = smem_u32(smem) + r * 16;
+    const uint32_t sc_base = smem_u32(smem_sc) + r * 4;
+    for (int j = xw; j < total; j += kFXformWG) {
+      const int stage = j % kFStages, as = j % kFNA;
+      mbar_wait(&full[stage], (j / kFStages) & 1);
+      uint4 q[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) q[c] = ld_shared_v4(w_base + stage * kFStage + c * (kTileN * 16));
+      const int32_t k = static_cast<int32_t>(ld_shared_u32(sc_base + stage * kTileN * 4));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      const float kf = static_cast<float>(k);
+      const uint32_t k1 = half2_bits(kf);
+      const uint32_t k16 = half2_bits(kf * 0.0625f);
+      const uint32_t cA = half2_bits(1536.0f - 1032.0f * kf);
+      const uint32_t cB = half2_bits(1536.0f - 72.0f * kf);
+      uint32_t a[32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t w4[4] = {q[c].x, q[c].y, q[c].z, q[c].w};
+#pragma unroll
+        for (int w = 0; w < 4; ++w) fold_word(w4[w], k1, k16, cA, cB, a[c * 8 + 2 * w], a[c * 8 + 2 * w + 1]);
+      }
+      mbar_wait(&a_empty[as], ((j / kFNA) & 1) ^ 1);
+      tc_fence_after();
+      tmem_st_x32(tmem_base + lane_base + as * 32, a);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_full[as]);
+    }
+  } else if (warp >= 4 + 4 * kFXformWG) {
+    // ---------------------------------------------------------------- epilogue
+    const uint32_t ew = warp - (4 + 4 * kFXformWG);
+    const uint32_t t128 = ew * 32 + lane;
+    const uint32_t r = t128;                      // TMEM lane == channel in tile
+    const uint32_t lane_base = (ew * 32) << 16;
+    pdl_wait();  // sa / out may be touched by the preceding grid
+    auto sa_prefetch = [&](int it) {
+      if (it < ntiles) {
+        int nt, mt;
+        tile_of(it, nt, mt);
+        for (int t = t128; t < kFMT; t += 128) {
+          const int64_t m = static_cast<int64_t>(mt) * kFMT + t;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                           smem_u32(sa_s + (it & 1) * kFMT + t)),
+                       "l"(p.sa + (m < p.M ? m : 0)), "r"(m < p.M ? 8 : 0)
+                       : "memory");
+        }
+      }
+      cp_async_commit();
+    };
+    sa_prefetch(0);
+    for (int it = 0; it < ntiles; ++it) {
+      int nt, mt;
+      tile_of(it, nt, mt);
+      const int ds = it & 1;
+      sa_prefetch(it + 1);
+      cp_async_wait<1>();
+      named_bar_sync(1, 128);  // sa_s[it & 1] complete for all epilogue threads
+      const double* sa_t = sa_s + (it & 1) * kFMT;
+      mbar_wait(&d_full[ds], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + lane_base + kFDCol + ds * kFMT;
+      const int64_t n = static_cast<int64_t>(nt) * kTileN + r;
+      const int64_t m0 = static_cast<int64_t>(mt) * kFMT;
+#pragma unroll 1
+      for (int cc = 0; cc < kFMT; cc += 32) {
+        uint32_t v[32];
+        tmem_ld_x16_(taddr + cc, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+        tmem_ld_x16_(taddr + cc + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+        tmem_wait_ld();
+        if (cc + 32 >= kFMT) {  // all of D[ds] read: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d_empty[ds]);
+        }
+        if (n < p.N) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int64_t m = m0 + cc + t;
+            if (m < p.M) {
+              const double o = __dmul_rn(static_cast<double>(static_cast<int32_t>(v[t])) * p.inv_amp,
+                                         sa_t[cc + t]);
+              store_out_f(p.out, p.out_dtype, m * p.N + n, __double2float_rn(o));
+            }
+          }
+        }
+      }
+      named_bar_sync(1, 128);  // done with sa_s[it & 1] before it is refilled
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
+}  // namespace
+
+bool fold_eligible(int64_t m, const isb_weight& w, int path) {
+  return path == ISB_PATH_INTEGER_SCALE && w.has_int_scales && w.tensor_core_ok() &&
+         w.max_int_scale >= 1 && w.max_int_scale <= 16 && m >= kFoldMinM;
+}
+
+void launch_gemm_fold(const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
+                      void* out, int out_dtype, int num_sms, cudaStream_t s) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cuda_check(cudaFuncSetAttribute(gemm_w4a8_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kFSmem),
+               "cudaFuncSetAttribute(fold smem)");
+  });
+  FoldParams prm{};
+  prm.packed = w.packed;
+  prm.kscale = w.kscale_tiled;
+  prm.sa = sa;
+  prm.out = out;
+  prm.M = static_cast<int>(m);
+  prm.N = static_cast<int>(w.n);
+  prm.G = static_cast<int>(w.groups);
+  prm.gb = static_cast<int>(w.group / kBlockK);
+  prm.kblocks = static_cast<int>(w.kblocks);
+  prm.m_tiles = static_cast<int>((m + kFMT - 1) / kFMT);
+  prm.tiles = static_cast<int>(w.n_tiles) * prm.m_tiles;
+  prm.out_dtype = out_dtype;
+  prm.inv_amp = std::ldexp(1.0, -w.exponent);
+  const CUtensorMap map = make_x_map(xq, m, w.k, kFMT);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min(prm.tiles, num_sms));
+  cfg.blockDim = dim3(kFThreads);
+  cfg.dynamicSmemBytes = kFSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, gemm_w4a8_fold, map, prm), "gemm_w4a8_fold launch");
+  count_launch();
+}
+
+}  // namespace isb

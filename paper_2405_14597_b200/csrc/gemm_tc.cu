@@ -587,36 +587,6 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem_base, Cf::kTmemCols);
 }
 
-// ---------------------------------------------------------------------------- host side
-PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaDriverEntryPointQueryResult q{};
-    void* f = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  });
-  if (!fn) fail(ISB_CUDA, "cuTensorMapEncodeTiled unavailable");
-  return fn;
-}
-
-CUtensorMap make_x_map(const int8_t* xq, int64_t m, int64_t k, int mt) {
-  CUtensorMap map;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(m)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(k)};
-  const cuuint32_t box[2] = {128u, static_cast<cuuint32_t>(mt)};
-  const cuuint32_t estr[2] = {1u, 1u};
-  const CUresult r = get_encode_fn()(
-      &map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(xq), dims, strides, box, estr,
-      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) fail(ISB_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
-  return map;
-}
-
 template <int MT, int PATH, bool GB1>
 void prepare_kernel() {
   static std::once_flag once;
@@ -703,6 +673,37 @@ int cluster_capacity(int mt, int C) {
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------------------- host side (shared)
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q{};
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  if (!fn) fail(ISB_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap make_x_map(const int8_t* xq, int64_t m, int64_t k, int mt) {
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(m)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(k)};
+  const cuuint32_t box[2] = {128u, static_cast<cuuint32_t>(mt)};
+  const cuuint32_t estr[2] = {1u, 1u};
+  const CUresult r = get_encode_fn()(
+      &map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(xq), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(ISB_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return map;
+}
+
 
 GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path) {
   (void)path;

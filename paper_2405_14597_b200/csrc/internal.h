@@ -5,6 +5,7 @@
 #include <stdexcept>
 #include <string>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/intscale_b200.h"
@@ -70,6 +71,13 @@ extern int64_t* g_trace;  // debug timeline buffer (8 x 512 int64), nullptr = of
 extern int g_trace_cta;
 extern int g_dbg;
 GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path);
+// 2-D TMA map over int8 activations [m][k], box 128 (K) x mt (rows), SWIZZLE_128B.
+CUtensorMap make_x_map(const int8_t* xq, int64_t m, int64_t k, int mt);
+// Prefill K3 with k_g folded into the weight expansion (gemm_fold.cu).
+constexpr int64_t kFoldMinM = 256;
+bool fold_eligible(int64_t m, const isb_weight& w, int path);
+void launch_gemm_fold(const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
+                      void* out, int out_dtype, int num_sms, cudaStream_t s);
 void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                     void* out, int out_dtype, void* workspace, const GemmPlan& plan,
                     cudaStream_t s);

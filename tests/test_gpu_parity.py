@@ -229,3 +229,57 @@ def test_checked_overflow_rig():
     assert np.array_equal(out.cpu().numpy().view(np.int32), ref.output.view(np.int32))
     with pytest.raises(isb.OverflowError_, match=r"\(0, 0\)"):
         isb.gemm_checked("integer-scale", xq, sa, pw, strict=True)
+
+
+# ------------------------------------------------------------------------- K3 prefill (k_g folded)
+FOLD_SHAPES = [(256, 1024, 256), (300, 1024, 384), (512, 2048, 640), (448, 11008, 128),
+               (1000, 512, 1000), (777, 4096, 130)]
+
+
+@pytest.mark.parametrize("m,k,n", FOLD_SHAPES)
+def test_fold_prefill_bit_exact(m, k, n):
+    """M >= 256 with k_g <= 16 runs the folded kernel (k_g * w expanded into the int8
+    operand, whole-K accumulation in TMEM): float32 output 0 ULP, bf16 = RN(f32)."""
+    x, w, s, _, _ = llama_problem(m, k, n, seed_w=100 + n, seed_x=200 + m)
+    assert s.int_scales.max() <= 16
+    ref = O.gemm_integer_scale(x, w, s)
+    pw = pack(w, s)
+    xq, sa = dev(x.values, torch.int8), dev(x.scales)
+    out32 = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.float32)
+    outbf = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.bfloat16)
+    out16 = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.float16)
+    torch.cuda.synchronize()
+    got = out32.cpu().numpy()
+    assert np.array_equal(got.view(np.int32), ref.output.view(np.int32)), \
+        f"max ulp {O.ulp_distance(got, ref.output).max()}"
+    assert np.array_equal(outbf.float().cpu().numpy(), to_bf16_np(ref.output))
+    assert np.array_equal(out16.float().cpu().numpy(),
+                          torch.from_numpy(ref.output).half().float().numpy())
+
+
+def test_fold_extreme_codes_and_k16():
+    """The fold's edge: k_g = 16 with codes -8 and 7 (k*w = -128 / 112) and extreme
+    activations (+-127), all in one tile, against the oracle."""
+    m, k, n, g = 300, 512, 256, 128
+    rng = np.random.default_rng(11)
+    codes = rng.integers(-8, 8, size=(k, n)).astype(np.int16)
+    codes[:64, :] = -8
+    codes[64:128, :] = 7
+    groups = k // g
+    amp = 1024
+    ks = rng.integers(1, 17, size=(n, groups))
+    ks[:, 0] = 16
+    scales = (ks / amp).astype(np.float64).reshape(-1)
+    w = O.QuantizedTensor(codes, 4, O.SYMMETRIC, O.GROUP, g, scales, np.zeros(0, np.int32))
+    s = O.integerize_scales(scales, amp)
+    assert s.int_scales.max() == 16
+    xv = rng.integers(-127, 128, size=(m, k)).astype(np.int16)
+    xv[0, :] = 127
+    xv[1, :] = -127
+    x = O.QuantizedTensor(xv, 8, O.SYMMETRIC, O.PER_TOKEN, 0,
+                          rng.uniform(1e-3, 1e-1, size=m).astype(np.float64), np.zeros(0, np.int32))
+    assert O.overflow_analyzer(k, g, 8, 4, s)["safe"]
+    ref = O.gemm_integer_scale(x, w, s)
+    out = isb.gemm_integer_scale(dev(x.values, torch.int8), dev(x.scales), pack(w, s),
+                                 out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(out.view(np.int32), ref.output.view(np.int32))
