@@ -78,6 +78,18 @@ ISB_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
       "r"(parity)
       : "memory");
+#elif defined(ISB_WAIT_HINT)
+  // Suspend-time hint: a waiting warp sleeps in the instruction (woken when the
+  // phase completes) instead of re-issuing TRYWAIT in a hot loop.
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(addr),
+      "r"(parity), "r"(ISB_WAIT_HINT)
+      : "memory");
 #else
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"

@@ -78,6 +78,13 @@ constexpr int64_t kFoldMinM = 256;
 bool fold_eligible(int64_t m, const isb_weight& w, int path);
 void launch_gemm_fold(const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                       void* out, int out_dtype, int num_sms, cudaStream_t s);
+// Decode K3d/K4d (gemm_decode.cu): stream-K over all SMs, two CTAs per SM.
+constexpr int64_t kDecodeMaxM = 32;
+bool decode_eligible(int64_t m, const isb_weight& w);
+int64_t decode_workspace_bytes(int64_t m, const isb_weight& w);
+void launch_gemm_decode(int path, const int8_t* xq, const double* sa, int64_t m,
+                        const isb_weight& w, void* out, int out_dtype, void* workspace,
+                        int num_sms, cudaStream_t s);
 void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                     void* out, int out_dtype, void* workspace, const GemmPlan& plan,
                     cudaStream_t s);

@@ -11,7 +11,8 @@ import paper_2405_14597_b200 as isb  # noqa: E402
 dev = torch.device("cuda:0")
 gen = torch.Generator(device=dev)
 gen.manual_seed(0)
-for (m, k, n) in [(16, 4096, 4096), (16, 4096, 22016)]:
+shapes = [(16, 4096, 4096), (16, 4096, 22016)] + ([(16, 4096, 131072)] if os.environ.get('BIG') else [])
+for (m, k, n) in shapes:
     ws = []
     for _ in range(3):
         wf = bench.llama_like_weight(k, n, gen, dev)
@@ -41,4 +42,5 @@ for (m, k, n) in [(16, 4096, 4096), (16, 4096, 22016)]:
     e1.record()
     torch.cuda.synchronize()
     graph = e0.elapsed_time(e1) * 1000 / 60
-    print(f"PDL={os.environ.get('ISB_NO_PDL') != '1'} M={m} K={k} N={n}: eager {eager:.2f} us, graph {graph:.2f} us")
+    gb = (n * k // 2 + 4 * n * k // 128) / graph / 1e3
+    print(f"{gb:.0f} GB/s PDL={os.environ.get('ISB_NO_PDL') != '1'} M={m} K={k} N={n}: eager {eager:.2f} us, graph {graph:.2f} us")

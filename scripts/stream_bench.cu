@@ -102,14 +102,13 @@ int main() {
   cudaMemset(buf, 1, total);
   cudaMalloc(&sink, 4);
   run_bulk<8192, 4, 1, true>(buf, total, sink);
-  run_bulk<8192, 12, 1, true>(buf, total, sink);
+  run_bulk<8192, 6, 1, true>(buf, total, sink);
+  run_bulk<8192, 6, 1, false>(buf, total, sink);
+  run_bulk<8192, 8, 1, false>(buf, total, sink);
   run_bulk<8192, 12, 1, false>(buf, total, sink);
-  run_bulk<8192, 20, 1, false>(buf, total, sink);
-  run_bulk<2048, 12, 4, false>(buf, total, sink);
+  run_bulk<8192, 16, 1, false>(buf, total, sink);
+  run_bulk<16384, 6, 1, false>(buf, total, sink);
   run_bulk<16384, 8, 1, false>(buf, total, sink);
-  run_bulk<32768, 4, 1, false>(buf, total, sink);
-  run_bulk<4096, 32, 1, false>(buf, total, sink);
-  run_bulk<1024, 64, 1, false>(buf, total, sink);
   {
     const int ctas = 148 * 2;
     const int64_t per = total / 16 / ctas;

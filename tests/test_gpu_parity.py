@@ -187,8 +187,44 @@ def test_workspace_is_left_clean_and_results_repeat():
         b = isb.gemm_integer_scale(xq, sa, pw, torch.float32, workspace=ws)
         assert torch.equal(a, b)
     torch.cuda.synchronize()
-    tiles = (4096 + 127) // 128                                   # one m-tile at M=16
-    assert int(ws.buf[: 4 * tiles].view(torch.int32).abs().sum()) == 0  # counters reset
+    assert int(ws.buf.view(torch.int32).abs().sum()) == 0  # split-K workspace left clean
+
+
+def test_decode_stream_k_kernel_subprocess():
+    """The opt-in stream-K decode kernel (ISB_DECODE=1, read once per process):
+    bit-exact int32 / float32 on every split pattern, workspace left clean."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ISB_DECODE="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"),
+                        "-k", "test_decode_stream_k_bit_exact or workspace_is_left_clean"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("m", [1, 5, 16, 17, 32])
+@pytest.mark.parametrize("k,n,g", [(4096, 12288, 128), (11008, 4096, 128), (4096, 22016, 128),
+                                   (11008, 1000, 256), (2048, 640, 512), (256, 4, 128)])
+def test_decode_stream_k_bit_exact(m, k, n, g):
+    """Decode shapes on every LLaMA-2-7B linear plus ragged N / g > 128: int32 acc
+    and float32 output bit-exact for every split pattern (default cluster kernel;
+    the stream-K kernel when run under ISB_DECODE=1)."""
+    x, w, s, _, _ = llama_problem(m, k, n, seed_w=7 + n + g, seed_x=11 + m, g=g)
+    ref = O.gemm_integer_scale(x, w, s)
+    pw = pack(w, s)
+    xq, sa = dev(x.values, torch.int8), dev(x.scales)
+    ws = isb.Workspace()
+    for _ in range(2):  # second call reuses the workspace the first left clean
+        out = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.float32, workspace=ws)
+        got = out.cpu().numpy()
+        assert np.array_equal(got.view(np.int32), ref.output.view(np.int32))
+    outf = isb.gemm_float_scale(xq, sa, pw, out_dtype=torch.float32, workspace=ws)
+    rf = O.gemm_float_scale(x, w)
+    err = np.abs(outf.cpu().numpy().astype(np.float64) - rf.output_f64)
+    assert err.max() <= 1e-5 * np.abs(rf.output_f64).max() + 1e-30
 
 
 # ------------------------------------------------------------------------- checked kernel
