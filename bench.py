@@ -172,21 +172,30 @@ def build_layers(isb, m, dev, seed):
 
 # ----------------------------------------------------------------------------- ours
 class LayerStep:
-    """One step: K1 quantize + K3 (or K4) GEMM per linear of one layer replica.
-    Captured into a CUDA graph per replica (8 kernel nodes)."""
+    """One step: per-token quantization + integer-scale (or float-scale) GEMM for
+    every linear of one layer replica, captured into a CUDA graph per replica.
+    fused=True: one launch per linear (K1 fused into K3/K4, config C3);
+    fused=False: K1 then K3/K4 (two launches per linear)."""
 
-    def __init__(self, isb, layers, xs, m, path, dev):
+    def __init__(self, isb, layers, xs, m, path, dev, fused=False):
         import torch
         self.isb, self.layers, self.xs, self.m, self.path = isb, layers, xs, m, path
+        self.fused = fused
         self.q = [torch.empty((m, k), dtype=torch.int8, device=dev) for _, k, _ in LAYER]
         self.sa = [torch.empty((m,), dtype=torch.float64, device=dev) for _ in LAYER]
         self.out = [torch.empty((m, n), dtype=torch.bfloat16, device=dev) for _, _, n in LAYER]
         self.ws = [isb.Workspace() for _ in range(REPLICAS)]
         self.graphs = []
-        self.kernels_per_step = 2 * len(LAYER)
+        self.kernels_per_step = (1 if fused else 2) * len(LAYER)
 
     def run_eager(self, r):
         isb = self.isb
+        if self.fused:
+            path = "integer-scale" if self.path == "int" else "float-scale"
+            for i, (_, k, n, w, _) in enumerate(self.layers[r]):
+                isb.gemm_act_fused(self.xs[i], w, path=path, out=self.out[i],
+                                   sa_out=self.sa[i], workspace=self.ws[r])
+            return
         gemm = isb.gemm_integer_scale if self.path == "int" else isb.gemm_float_scale
         for i, (_, k, n, w, _) in enumerate(self.layers[r]):
             q, sa = self.q[i], self.sa[i]
@@ -292,6 +301,10 @@ def run_ours(args, ws, rank, local):
     fstep = LayerStep(isb, layers, xs, m, "float", dev)
     fstep.capture()
     fms = max_over_ranks(time_steps(fstep.replay, args.steps, args.warmup, ws), ws) / args.steps
+    # ---- the same step with K1 fused into the GEMM (one launch per linear, config C3)
+    fzstep = LayerStep(isb, layers, xs, m, "int", dev, fused=True)
+    fzstep.capture()
+    fzms = max_over_ranks(time_steps(fzstep.replay, args.steps, args.warmup, ws), ws) / args.steps
 
     # ---- e2e: host pinned X in, host bf16 out, through the public API every step
     xh = [x.cpu().pin_memory() for x in xs]
@@ -373,6 +386,7 @@ def run_ours(args, ws, rank, local):
         },
         "speedup_vs_float_scale": round(fms / ms_per_step, 3),
         "float_scale_us_per_layer": round(fms * 1e3, 2),
+        "act_fused_us_per_layer": round(fzms * 1e3, 2),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic,

@@ -41,7 +41,10 @@ enum isb_status {
   ISB_CUDA = 8       /* CUDA runtime / launch failure (no reference analogue) */
 };
 
-enum isb_dtype { ISB_F32 = 0, ISB_BF16 = 1, ISB_F16 = 2 };
+/* ISB_I32 (GEMM output only, integer-scale path): the raw int32 scaled
+ * accumulator acc = sum_g P_g * k_g, before the Eq. 2 epilogue — the value a
+ * row-parallel (K-sharded) layer all-reduces exactly; see isb_finalize_acc. */
+enum isb_dtype { ISB_F32 = 0, ISB_BF16 = 1, ISB_F16 = 2, ISB_I32 = 3 };
 
 enum isb_path { ISB_PATH_FLOAT_SCALE = 0, ISB_PATH_INTEGER_SCALE = 1 };
 
@@ -129,6 +132,38 @@ int isb_gemm_integer_scale(const int8_t* xq, const double* sa, int64_t m, int64_
 int isb_gemm_float_scale(const int8_t* xq, const double* sa, int64_t m, int64_t k,
                          const isb_weight* w, void* out, int out_dtype, void* workspace,
                          int64_t workspace_bytes, void* stream);
+
+/* --------------------------------------------------------------------------
+ * K1 (+) K3/K4 — per-token activation quantization fused into the GEMM
+ * (BASELINE config C3 "per-token act quant fused"): x is the float32 / bf16
+ * M x K activation; each CTA quantizes its K slice into shared memory with the
+ * full-row max combined across its cluster, so the codes and scales are exactly
+ * those of quantize(x, 8, symmetric, per_token) (quantize.cpp:93-145) and the
+ * output equals isb_quantize_per_token followed by isb_gemm_integer_scale /
+ * isb_gemm_float_scale, in one launch. sa_out (nullable) receives the per-token
+ * scales. Decode shapes (M <= 64) whose K slice fits run fused; anything else
+ * runs the two kernels back to back (same results).
+ */
+int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t k,
+                       const isb_weight* w, void* out, int out_dtype, double* sa_out,
+                       void* workspace, int64_t workspace_bytes, void* stream);
+
+/* --------------------------------------------------------------------------
+ * Tensor parallelism (no reference analogue — the reference is one
+ * host process). Row-parallel layers shard K on group boundaries: every rank
+ * produces the int32 accumulator of its groups (out_dtype = ISB_I32 above),
+ * the ranks all-reduce it (integer sum: exact and order-independent), and
+ * isb_finalize_acc applies Eq. 2 (gemm.cpp:252): out = float((acc / 2^e) * s_a).
+ * A K-sharded activation needs the FULL-row absmax for the per-token scale
+ * (quantize.cpp:120-125): isb_row_absmax gives each rank's partial max, the
+ * ranks all-reduce MAX, and isb_quantize_per_token_amax quantizes the local
+ * slice with that global max — codes bit-identical to quantizing the full row.
+ */
+int isb_finalize_acc(const int32_t* acc, const double* sa, int64_t m, int64_t n,
+                     int64_t amplifier, void* out, int out_dtype, void* stream);
+int isb_row_absmax(const void* x, int x_dtype, int64_t m, int64_t k, float* amax, void* stream);
+int isb_quantize_per_token_amax(const void* x, int x_dtype, int64_t m, int64_t k,
+                                const float* amax, int8_t* codes, double* scales, void* stream);
 
 /* --------------------------------------------------------------------------
  * Checked GEMM (CUDA cores, int64): the full reference semantics for any

@@ -195,7 +195,8 @@ void require_gemm_args(const int8_t* xq, const double* sa, int64_t m, int64_t k,
   if (k != w->k)
     fail(ISB_DIMENSION,
          "activation K=" + std::to_string(k) + " vs weight rows " + std::to_string(w->k));
-  if (out_dtype != ISB_F32 && out_dtype != ISB_BF16 && out_dtype != ISB_F16)
+  if (out_dtype != ISB_F32 && out_dtype != ISB_BF16 && out_dtype != ISB_F16 &&
+      out_dtype != ISB_I32)
     fail(ISB_PARAM, "unsupported output dtype");
 }
 
@@ -207,6 +208,8 @@ void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
     fail(ISB_PARAM, "tcgen05 path needs K % 128 == 0 and group % 128 == 0 (use isb_gemm_checked)");
   if (path == ISB_PATH_INTEGER_SCALE && !w->has_int_scales)
     fail(ISB_PARAM, "integer-scale path needs an IntegerScaleSet");
+  if (out_dtype == ISB_I32 && path != ISB_PATH_INTEGER_SCALE)
+    fail(ISB_PARAM, "raw int32 accumulator output exists only on the integer-scale path");
   if (m > std::numeric_limits<int>::max() || w->n > std::numeric_limits<int>::max())
     fail(ISB_PARAM, "shape too large");
   if (decode_eligible(m, *w) && !decode_disabled()) {
@@ -373,6 +376,77 @@ int isb_gemm_float_scale(const int8_t* xq, const double* sa, int64_t m, int64_t 
   return guarded([&] {
     gemm_tc(ISB_PATH_FLOAT_SCALE, xq, sa, m, k, w, out, out_dtype, workspace, workspace_bytes,
             stream);
+  });
+}
+
+int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t k,
+                       const isb_weight* w, void* out, int out_dtype, double* sa_out,
+                       void* workspace, int64_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    if (!w) fail(ISB_PARAM, "null weight handle");
+    if (!x || !out) fail(ISB_PARAM, "null pointer");
+    if (m < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+    if (k != w->k)
+      fail(ISB_DIMENSION,
+           "activation K=" + std::to_string(k) + " vs weight rows " + std::to_string(w->k));
+    if (x_dtype != ISB_F32 && x_dtype != ISB_BF16)
+      fail(ISB_PARAM, "activations must be float32 or bfloat16");
+    if (path != ISB_PATH_INTEGER_SCALE && path != ISB_PATH_FLOAT_SCALE)
+      fail(ISB_PARAM, "unknown path");
+    if (path == ISB_PATH_INTEGER_SCALE && !w->has_int_scales)
+      fail(ISB_PARAM, "integer-scale path needs an IntegerScaleSet");
+    if (out_dtype != ISB_F32 && out_dtype != ISB_BF16 && out_dtype != ISB_F16)
+      fail(ISB_PARAM, "unsupported output dtype");
+    cudaStream_t s = as_stream(stream);
+    const bool aligned = reinterpret_cast<uintptr_t>(x) % 16 == 0;
+    if (aligned && act_fused_eligible(m, k, *w)) {
+      const GemmPlan pl = plan_gemm(m, *w, num_sms(), path, true);
+      launch_gemm_tc(path, nullptr, nullptr, m, *w, out, out_dtype, workspace, pl, s, x, x_dtype,
+                     sa_out);
+      return;
+    }
+    // Unfused: K1 into stream-ordered temporaries, then the GEMM.
+    int8_t* codes = nullptr;
+    double* sa = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&codes), m * k, s), "cudaMallocAsync");
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&sa), m * sizeof(double), s),
+               "cudaMallocAsync");
+    launch_quantize_per_token(x, x_dtype, m, k, codes, sa, scratch_flag(), s);
+    if (sa_out)
+      cuda_check(cudaMemcpyAsync(sa_out, sa, m * sizeof(double), cudaMemcpyDeviceToDevice, s),
+                 "copy scales");
+    gemm_tc(path, codes, sa, m, k, w, out, out_dtype, workspace, workspace_bytes, stream);
+    cudaFreeAsync(codes, s);
+    cudaFreeAsync(sa, s);
+  });
+}
+
+int isb_finalize_acc(const int32_t* acc, const double* sa, int64_t m, int64_t n,
+                     int64_t amplifier, void* out, int out_dtype, void* stream) {
+  return guarded([&] {
+    if (!acc || !sa || !out) fail(ISB_PARAM, "null pointer");
+    if (m < 1 || n < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+    if (out_dtype != ISB_F32 && out_dtype != ISB_BF16 && out_dtype != ISB_F16)
+      fail(ISB_PARAM, "unsupported output dtype");
+    const int e = exponent_of(amplifier);
+    launch_finalize_acc(acc, sa, m, n, std::ldexp(1.0, -e), out, out_dtype, as_stream(stream));
+  });
+}
+
+int isb_row_absmax(const void* x, int x_dtype, int64_t m, int64_t k, float* amax, void* stream) {
+  return guarded([&] {
+    if (!x || !amax) fail(ISB_PARAM, "null pointer");
+    if (m < 1 || k < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+    launch_row_absmax(x, x_dtype, m, k, amax, as_stream(stream));
+  });
+}
+
+int isb_quantize_per_token_amax(const void* x, int x_dtype, int64_t m, int64_t k,
+                                const float* amax, int8_t* codes, double* scales, void* stream) {
+  return guarded([&] {
+    if (!x || !amax || !codes || !scales) fail(ISB_PARAM, "null pointer");
+    if (m < 1 || k < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+    launch_quantize_amax(x, x_dtype, m, k, amax, codes, scales, as_stream(stream));
   });
 }
 

@@ -117,6 +117,7 @@ struct DParams {
   } while (0)
 
 __device__ __forceinline__ void store_out_d(void* out, int dtype, int64_t idx, float f) {
+  if (dtype == ISB_I32) return;  // raw accumulators are stored by store_acc_or_out
   if (dtype == ISB_F32)
     static_cast<float*>(out)[idx] = f;
   else if (dtype == ISB_BF16)
@@ -133,6 +134,16 @@ __device__ __forceinline__ float finish_d(uint32_t accbits, double sa, double in
   else                                 // Eq. 1: acc already carries s_g
     o = __dmul_rn(static_cast<double>(__uint_as_float(accbits)), sa);
   return __double2float_rn(o);
+}
+
+// Eq. 2 / Eq. 1 epilogue store, or the raw int32 accumulator (ISB_I32, row-parallel TP).
+template <int PATH>
+__device__ __forceinline__ void store_acc_or_out(const DParams& p, int64_t idx, uint32_t accbits,
+                                                 double sa) {
+  if (PATH == ISB_PATH_INTEGER_SCALE && p.out_dtype == ISB_I32)
+    static_cast<uint32_t*>(p.out)[idx] = accbits;
+  else
+    store_out_d(p.out, p.out_dtype, idx, finish_d<PATH>(accbits, sa, p.inv_amp));
 }
 
 // Number of CTAs whose range touches tile t (each contributes one segment).
@@ -443,11 +454,11 @@ __global__ void __launch_bounds__(DCfg<MT>::kThreads, DCfg<MT>::kMinBlocks)
 #pragma unroll
           for (int m = 0; m < MT; ++m)
             if (m < p.M)
-              store_out_d(p.out, p.out_dtype, static_cast<int64_t>(m) * p.N + nn,
-                          finish_d<PATH>(PATH == ISB_PATH_INTEGER_SCALE
-                                             ? static_cast<uint32_t>(iacc[m])
-                                             : __float_as_uint(facc[m]),
-                                         ssa[m], p.inv_amp));
+              store_acc_or_out<PATH>(p, static_cast<int64_t>(m) * p.N + nn,
+                                     PATH == ISB_PATH_INTEGER_SCALE
+                                         ? static_cast<uint32_t>(iacc[m])
+                                         : __float_as_uint(facc[m]),
+                                     ssa[m]);
         }
       } else {
         // Publish [MT][128] x 32-bit into staging slot pidx & 1 (owned by fix-up
@@ -536,8 +547,8 @@ __global__ void __launch_bounds__(DCfg<MT>::kThreads, DCfg<MT>::kMinBlocks)
 #pragma unroll
             for (int e = 0; e < 4; ++e)
               if (n0 + e < p.N)
-                store_out_d(p.out, p.out_dtype, static_cast<int64_t>(i0 + i) * p.N + n0 + e,
-                            finish_d<PATH>(vv[e], ssa[i0 + i], p.inv_amp));
+                store_acc_or_out<PATH>(p, static_cast<int64_t>(i0 + i) * p.N + n0 + e, vv[e],
+                                       ssa[i0 + i]);
           }
         }
       }

@@ -305,9 +305,13 @@ __global__ void __launch_bounds__(kFThreads, 1)
           for (int t = 0; t < 32; ++t) {
             const int64_t m = m0 + cc + t;
             if (m < p.M) {
-              const double o = __dmul_rn(static_cast<double>(static_cast<int32_t>(v[t])) * p.inv_amp,
-                                         sa_t[cc + t]);
-              store_out_f(p.out, p.out_dtype, m * p.N + n, __double2float_rn(o));
+              if (p.out_dtype == ISB_I32) {  // raw acc (row-parallel TP)
+                static_cast<int32_t*>(p.out)[m * p.N + n] = static_cast<int32_t>(v[t]);
+              } else {
+                const double o = __dmul_rn(
+                    static_cast<double>(static_cast<int32_t>(v[t])) * p.inv_amp, sa_t[cc + t]);
+                store_out_f(p.out, p.out_dtype, m * p.N + n, __double2float_rn(o));
+              }
             }
           }
         }

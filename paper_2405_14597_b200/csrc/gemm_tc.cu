@@ -41,6 +41,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "layout.cuh"
+#include "quant.cuh"
 
 namespace isb {
 
@@ -51,7 +52,12 @@ int g_dbg = 0;
 namespace {
 
 
-template <int MT>
+// XQ: per-token activation quantization fused into the GEMM (config C3). The CTA
+// quantizes the float activation slice of its K range (its cluster rank's
+// groups) straight into a resident SWIZZLE_128B smem region; the full-row absmax
+// the per-token scale needs (quantize.cpp:120-125) is combined across the
+// cluster's ranks over DSMEM (the ranks of a cluster cover all of K).
+template <int MT, bool XQ = false>
 struct Cfg {
   static constexpr int S = MT <= 32 ? 4 : (MT == 64 ? 2 : 1);    // 128-K blocks per step
   static constexpr int kXformWG = MT >= 128 ? 1 : 2;             // transform warpgroups
@@ -67,7 +73,11 @@ struct Cfg {
                                    : kTmemUsed <= 128 ? 128 : kTmemUsed <= 256 ? 256 : 512;
   static_assert(kTmemUsed <= 512, "TMEM overflow");
   static constexpr int kXBytes = MT * 128;
-  static constexpr int kXSlot = kXBytes < 1024 ? 1024 : kXBytes;
+  static constexpr int kXTile = kXBytes < 1024 ? 1024 : kXBytes;  // SW128 tile stride
+  static constexpr int kXSlot = XQ ? 0 : kXTile;                  // per-step activation slots
+  static constexpr int kXRes = XQ ? 64 * 1024 : 0;                // resident quantized slice
+  static constexpr int kXResBlocks = XQ ? kXRes / kXTile : 0;
+  static constexpr int kAmaxBytes = XQ ? 8 * MT * 4 + MT * 4 + MT * 8 : 0;  // peers, local, s_a
   static constexpr int kScBytes = S * kTileN * 4;     // group scales riding with the step
   static constexpr int kStageBytes = S * (kBlockBytes + kXSlot) + kScBytes;
   // Tile partials handed from the epilogue to the reduction warps (2/3), which do
@@ -76,7 +86,8 @@ struct Cfg {
   static constexpr int kPbufs = MT <= 32 ? 2 : (MT == 64 ? 1 : 0);
   static constexpr int kPbufBytes = kPbufs * MT * kTileN * 4;
   static constexpr int kSaBytes = 2 * MT * 8;  // token scales, prefetched a tile ahead
-  static constexpr int kFixed = 1024 + kPbufBytes + kSaBytes + 1024;
+  static constexpr int kFixed = 1024 + kXRes + kPbufBytes + kSaBytes + kAmaxBytes + 1024;
+  static_assert(!XQ || kPbufs > 0, "fused activation quantization: decode tiles only");
   static constexpr int kStagesRaw = (227 * 1024 - kFixed) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kSmemBytes = kFixed + kStages * kStageBytes;
@@ -97,6 +108,10 @@ struct Params {
   int64_t* trace;         // optional debug timeline (see ISB_TRACE)
   int trace_cta;
   int dbg;                // debug knobs: 1 skip A st, 2 skip D ld, 4 skip MMA issue
+  const void* xf;         // XQ: float32 / bf16 activations [M][K]
+  int x_dtype;
+  int K;
+  double* sa_out;         // XQ: optional per-token scales out [M] (written by rank 0)
 };
 
 // Debug timeline: trace[role * 512 + i] = globaltimer at event i of that role.
@@ -167,8 +182,12 @@ __device__ __forceinline__ void reduce_tile(const Params& p, uint32_t pb, const 
           else fs += __uint_as_float(v[i][q]);
         }
         const int64_t m = static_cast<int64_t>(mt) * MT + lo + c0 + i;
-        if (n < p.N && m < p.M)
-          store_out(p.out, p.out_dtype, m * p.N + n, finish<PATH>(is, fs, sav[i], p.inv_amp));
+        if (n < p.N && m < p.M) {
+          if (PATH == ISB_PATH_INTEGER_SCALE && p.out_dtype == ISB_I32)
+            static_cast<int32_t*>(p.out)[m * p.N + n] = is;  // raw acc (row-parallel TP)
+          else
+            store_out(p.out, p.out_dtype, m * p.N + n, finish<PATH>(is, fs, sav[i], p.inv_amp));
+        }
       }
     }
   }
@@ -190,10 +209,10 @@ struct Work {
   __device__ int tile(int it, const Params& p) const { return cid + it * p.NC; }
 };
 
-template <int MT, int PATH, bool GB1>
-__global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
+template <int MT, int PATH, bool GB1, bool XQ>
+__global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
     gemm_w4a8_tc(const __grid_constant__ CUtensorMap x_map, const Params p) {
-  using Cf = Cfg<MT>;
+  using Cf = Cfg<MT, XQ>;
   constexpr int S = Cf::S;
   constexpr int kStages = Cf::kStages;
   constexpr int kXSlot = Cf::kXSlot;
@@ -201,12 +220,17 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* smem_w = smem;                                        // [stage][S][8 KiB]
-  uint8_t* smem_x = smem + kStages * S * kBlockBytes;            // [stage][S][kXSlot]
+  uint8_t* smem_xres = smem;                                     // XQ: [kb][MT rows][128 B]
+  uint8_t* smem_w = smem + Cf::kXRes;                            // [stage][S][8 KiB]
+  uint8_t* smem_x = smem_w + kStages * S * kBlockBytes;          // [stage][S][kXSlot]
   uint8_t* smem_sc = smem_x + kStages * S * kXSlot;              // [stage][S][128] scales
   uint8_t* pbuf = smem_sc + kStages * Cf::kScBytes;              // [kPbufs][MT][128] partials
   double* sa_s = reinterpret_cast<double*>(pbuf + Cf::kPbufBytes);  // [2][MT]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + Cf::kPbufBytes + Cf::kSaBytes);
+  float* amx_peer = reinterpret_cast<float*>(pbuf + Cf::kPbufBytes + Cf::kSaBytes);  // XQ [8][MT]
+  float* amx_loc = amx_peer + 8 * MT;                                 // XQ [MT]
+  double* sa_f = reinterpret_cast<double*>(amx_loc + MT);             // XQ [MT] fused s_a
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + Cf::kPbufBytes + Cf::kSaBytes +
+                                               Cf::kAmaxBytes);
   uint64_t* full = bars;
   uint64_t* empty = full + kStages;
   uint64_t* a_full = empty + kStages;
@@ -217,7 +241,9 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
   uint64_t* pb_full = sc_empty + kStages;   // [2] epilogue -> reduction warps (local)
   uint64_t* red_full = pb_full + 2;         // [2] all ranks' partials published (cluster)
   uint64_t* red_empty = red_full + 2;       // [2] all ranks done reading ours (cluster)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_empty + 2);
+  uint64_t* x_ready = red_empty + 2;        // XQ: resident codes + s_a written (local)
+  uint64_t* amax_bar = x_ready + 1;         // XQ: all ranks' partial row maxima in (cluster)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(amax_bar + 1);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -225,7 +251,9 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
   const int nsteps = wk.nsteps_tile * wk.ntiles;
 
   if (warp == 0 && lane == 0) {
-    prefetch_tensormap(&x_map);
+    if (!XQ) prefetch_tensormap(&x_map);
+    mbar_init(x_ready, 1);
+    mbar_init(amax_bar, p.C);
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1 + 4);
@@ -277,7 +305,7 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
         step_range(j, tile, kb, nkb);
         const int nt = tile / p.m_tiles;
         const int ga = kb / p.gb, gz = (kb + nkb - 1) / p.gb;
-        mbar_arrive_expect_tx(&full[stage], nkb * (kBlockBytes + Cf::kXBytes) +
+        mbar_arrive_expect_tx(&full[stage], nkb * (kBlockBytes + (XQ ? 0 : Cf::kXBytes)) +
                                                 (gz - ga + 1) * kTileN * 4);
         bulk_load_evict_first(smem_w + stage * S * kBlockBytes,
                               p.packed + (static_cast<int64_t>(nt) * p.kblocks + kb) * kBlockBytes,
@@ -299,9 +327,11 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
           mbar_wait(&sc_empty[stage], ((j / kStages) & 1) ^ 1);
           load_static(j, stage);
         }
-        for (int i = 0; i < nkb; ++i)
-          tma_load_2d(smem_x + (stage * S + i) * kXSlot, &x_map, &full[stage], (kb + i) * kBlockK,
-                      mt * MT);
+        if (!XQ)
+          for (int i = 0; i < nkb; ++i)
+            tma_load_2d(smem_x + (stage * S + i) * kXSlot, &x_map, &full[stage],
+                        (kb + i) * kBlockK, mt * MT);
+        (void)mt;
         ISB_TRACE(0, j);
       }
     }
@@ -311,6 +341,8 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
     constexpr uint32_t idesc = make_idesc_i8(128, MT);
     const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
     const uint32_t x_base = smem_u32(smem_x);
+    const uint32_t xres_base = smem_u32(smem_xres);
+    if (XQ && nsteps > 0) mbar_wait(x_ready, 0);  // resident quantized activations written
     for (int j = 0; j < nsteps; ++j) {
       const int stage = j % kStages, as = j % Cf::kNA, ds = j % Cf::kND;
       int tile, kb, nkb;
@@ -323,7 +355,8 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
 #pragma unroll
       for (int i = 0; i < S; ++i) {
         if (i < nkb) {
-          const uint64_t bdesc = make_sw128_kmajor_desc(x_base + (stage * S + i) * kXSlot);
+          const uint64_t bdesc = make_sw128_kmajor_desc(
+              XQ ? xres_base + (kb + i - wk.kb0) * Cf::kXTile : x_base + (stage * S + i) * kXSlot);
           const uint32_t d_tmem = tbase + Cf::kNA * Cf::kACols + ds * Cf::kDCols + i * MT;
           const uint32_t a_tmem = tbase + as * Cf::kACols + i * 32;
 #pragma unroll
@@ -338,6 +371,131 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
       mma_commit_warp(&d_full[ds]);
     }
   } else if (warp >= 4 && warp < 4 + 4 * Cf::kXformWG) {
+    if constexpr (XQ) {
+      // ------------------------------------------------ fused per-token quantization
+      // quantize(x, 8, symmetric, per_token) (quantize.cpp:93-145) of this CTA's
+      // K slice [kb0, kb1) x 128, rows [0, MT) (decode: one token tile), into the
+      // resident SWIZZLE_128B layout the MMA reads (16 B chunk c of row r of a
+      // 128-K block lives at r*128 + ((c ^ (r & 7)) * 16)).
+      constexpr int kT = 128 * Cf::kXformWG;
+      constexpr int kTPR = kT / MT;  // threads per token row (consecutive lanes)
+      constexpr int kU = 4;          // 16-float chunks per thread kept in flight / registers
+      static_assert(kTPR >= 1 && kTPR <= 32 && (kTPR & (kTPR - 1)) == 0, "row mapping");
+      const int tid = static_cast<int>(threadIdx.x) - 128;
+      const int row = tid / kTPR, jr = tid % kTPR;
+      const int k0 = wk.kb0 * kBlockK, nblk = wk.kb1 - wk.kb0;
+      const int nch = nblk * 8;                      // 16-element chunks per row
+      const int mine = (nch - jr + kTPR - 1) / kTPR;  // chunks jr, jr + kTPR, ...
+      const bool live = row < p.M;
+      auto load_chunk = [&](int c, float (&v)[16]) {
+        const int64_t off = static_cast<int64_t>(row) * p.K + k0 + (c / 8) * kBlockK + (c % 8) * 16;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          float t4[4];
+          if (p.x_dtype == ISB_F32)
+            load4<float>(static_cast<const float*>(p.xf) + off + h * 4, t4);
+          else
+            load4<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(p.xf) + off + h * 4, t4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) v[h * 4 + e] = t4[e];
+        }
+      };
+      if (tid == 0) ISB_TRACE(9, 0);
+      pdl_wait();  // the activations may be produced by the preceding grid
+      if (tid == 0) ISB_TRACE(9, 1);
+      // pass 1: partial row max; the first kU chunks stay in registers for pass 2
+      float v0[kU][16];
+      float mx = 0.0f;
+      if (live) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (u < mine) load_chunk(jr + u * kTPR, v0[u]);
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (u < mine)
+#pragma unroll
+            for (int e = 0; e < 16; ++e) mx = fmaxf(mx, fabsf(v0[u][e]));
+        for (int u0 = kU; u0 < mine; u0 += kU) {
+          float vb[kU][16];
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+            if (u0 + u < mine) load_chunk(jr + (u0 + u) * kTPR, vb[u]);
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+            if (u0 + u < mine)
+#pragma unroll
+              for (int e = 0; e < 16; ++e) mx = fmaxf(mx, fabsf(vb[u][e]));
+        }
+      }
+#pragma unroll
+      for (int o = kTPR / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (jr == 0) amx_loc[row] = mx;
+      named_bar_sync(3, kT);
+      if (tid == 0) ISB_TRACE(9, 2);
+      if (p.C > 1) {
+        // every rank's partial maxima into every rank's amx_peer[rank][.] (DSMEM)
+        if (tid < p.C) {
+          const int q = tid;
+          for (int r = 0; r < MT; ++r)
+            asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(
+                             mapa_shared(smem_u32(amx_peer + wk.rank * MT + r), q)),
+                         "f"(amx_loc[r])
+                         : "memory");
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                           mapa_shared(smem_u32(amax_bar), q))
+                       : "memory");
+        }
+        mbar_wait_cluster(amax_bar, 0);
+      }
+      if (tid < MT) {
+        float a = amx_loc[tid];
+        if (p.C > 1) {
+          a = 0.0f;
+          for (int q = 0; q < p.C; ++q) a = fmaxf(a, amx_peer[q * MT + tid]);
+        }
+        const double sc = a == 0.0f ? 1.0 : static_cast<double>(a) / 127.0;  // quantize.cpp:120-125
+        sa_f[tid] = sc;
+        if (wk.rank == 0 && wk.cid == 0 && p.sa_out != nullptr && tid < p.M) p.sa_out[tid] = sc;
+      }
+      named_bar_sync(3, kT);
+      if (tid == 0) ISB_TRACE(9, 3);
+      // pass 2: codes into the resident tiles (16-byte chunk c of row r of block b at
+      // b*tile + r*128 + ((c ^ (r & 7)) * 16), the SWIZZLE_128B K-major layout)
+      const uint32_t xres = smem_u32(smem_xres);
+      const double sc = sa_f[row], rc = 1.0 / sc;
+      auto put_chunk = [&](int c, const float (&v)[16]) {
+        uint32_t w4[4] = {0u, 0u, 0u, 0u};
+        if (live) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            w4[e / 4] |= (static_cast<uint32_t>(quant_one(v[e], sc, rc, -128, 127)) & 0xFFu)
+                         << (8 * (e % 4));
+        }
+        const int b = c / 8, cb = c % 8;
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
+                         xres + b * Cf::kXTile + row * 128 + ((cb ^ (row & 7)) * 16)),
+                     "r"(w4[0]), "r"(w4[1]), "r"(w4[2]), "r"(w4[3])
+                     : "memory");
+      };
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (u < mine) put_chunk(jr + u * kTPR, v0[u]);
+      for (int u0 = kU; u0 < mine; u0 += kU) {
+        float vb[kU][16];
+        if (live) {
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+            if (u0 + u < mine) load_chunk(jr + (u0 + u) * kTPR, vb[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (u0 + u < mine) put_chunk(jr + (u0 + u) * kTPR, vb[u]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
+      named_bar_sync(3, kT);
+      if (tid == 0) mbar_arrive(x_ready);
+      if (tid == 0) ISB_TRACE(9, 4);
+    }
     // ---------------------------------------------------------------- transform
     const int xw = static_cast<int>(warp - 4) / 4;
     const uint32_t r = (warp % 4) * 32 + lane;  // output channel within the tile == TMEM lane
@@ -511,9 +669,13 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
 #pragma unroll
           for (int t = 0; t < kCols; ++t) {
             const int64_t m = static_cast<int64_t>(mt) * MT + c0 + t;
-            if (m < p.M)
-              store_out(p.out, p.out_dtype, m * p.N + n,
-                        finish<PATH>(iacc[t], facc[t], sa_t[c0 + t], p.inv_amp));
+            if (m < p.M) {
+              if (PATH == ISB_PATH_INTEGER_SCALE && p.out_dtype == ISB_I32)
+                static_cast<int32_t*>(p.out)[m * p.N + n] = iacc[t];
+              else
+                store_out(p.out, p.out_dtype, m * p.N + n,
+                          finish<PATH>(iacc[t], facc[t], sa_t[c0 + t], p.inv_amp));
+            }
           }
         }
       }
@@ -540,16 +702,19 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
         }
         cp_async_commit();
       };
-      sa_prefetch(0);
+      if (!XQ) sa_prefetch(0);
+      if (XQ && wk.ntiles > 0) mbar_wait(x_ready, 0);  // fused s_a in sa_f
       for (int it = 0; it < wk.ntiles; ++it) {
         const int buf = it % Cf::kPbufs;
         const uint32_t ph = (it / Cf::kPbufs) & 1;
         const int tile = wk.tile(it, p);
         const int nt = tile / p.m_tiles, mt = tile % p.m_tiles;
-        sa_prefetch(it + 1);
-        cp_async_wait<1>();
-        named_bar_sync(2, 64);  // sa_s[it & 1] visible to both reduction warps
-        const double* sa_t = sa_s + (it & 1) * MT;
+        if (!XQ) {
+          sa_prefetch(it + 1);
+          cp_async_wait<1>();
+          named_bar_sync(2, 64);  // sa_s[it & 1] visible to both reduction warps
+        }
+        const double* sa_t = XQ ? sa_f : sa_s + (it & 1) * MT;
         mbar_wait(&pb_full[buf], ph);
         if (p.C > 1) {
           if (lane < static_cast<uint32_t>(p.C))
@@ -564,7 +729,7 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
           case 4: reduce_tile<MT, 4, PATH>(p, pb, sa_t, wk.rank, nt, mt, u); break;
           default: reduce_tile<MT, 8, PATH>(p, pb, sa_t, wk.rank, nt, mt, u); break;
         }
-        named_bar_sync(2, 64);  // done with sa_s[it & 1] before it is refilled
+        if (!XQ) named_bar_sync(2, 64);  // done with sa_s[it & 1] before it is refilled
         if (warp == 2 && lane == 0) ISB_TRACE(7, it);
         if (p.C > 1) {
           if (lane < static_cast<uint32_t>(p.C))
@@ -587,13 +752,13 @@ __global__ void __launch_bounds__(Cfg<MT>::kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem_base, Cf::kTmemCols);
 }
 
-template <int MT, int PATH, bool GB1>
+template <int MT, int PATH, bool GB1, bool XQ>
 void prepare_kernel() {
   static std::once_flag once;
   std::call_once(once, [] {
-    auto kern = gemm_w4a8_tc<MT, PATH, GB1>;
+    auto kern = gemm_w4a8_tc<MT, PATH, GB1, XQ>;
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    Cfg<MT>::kSmemBytes),
+                                    Cfg<MT, XQ>::kSmemBytes),
                "cudaFuncSetAttribute(smem)");
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                "cudaFuncSetAttribute(cluster)");
@@ -601,13 +766,13 @@ void prepare_kernel() {
 }
 
 // Max co-resident clusters of size C for this kernel (driver occupancy query).
-template <int MT, int PATH, bool GB1>
+template <int MT, int PATH, bool GB1, bool XQ>
 int max_active_clusters(int C) {
-  prepare_kernel<MT, PATH, GB1>();
+  prepare_kernel<MT, PATH, GB1, XQ>();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(C * 64);
-  cfg.blockDim = dim3(Cfg<MT>::kThreads);
-  cfg.dynamicSmemBytes = Cfg<MT>::kSmemBytes;
+  cfg.blockDim = dim3(Cfg<MT, XQ>::kThreads);
+  cfg.dynamicSmemBytes = Cfg<MT, XQ>::kSmemBytes;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C;
@@ -616,17 +781,17 @@ int max_active_clusters(int C) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemm_w4a8_tc<MT, PATH, GB1>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_w4a8_tc<MT, PATH, GB1, XQ>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
   return n;
 }
 
-template <int MT, int PATH, bool GB1>
+template <int MT, int PATH, bool GB1, bool XQ>
 void launch_mt(const CUtensorMap& map, const Params& prm, int grid, cudaStream_t s) {
-  using Cf = Cfg<MT>;
-  prepare_kernel<MT, PATH, GB1>();
+  using Cf = Cfg<MT, XQ>;
+  prepare_kernel<MT, PATH, GB1, XQ>();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(Cf::kThreads);
@@ -641,7 +806,7 @@ void launch_mt(const CUtensorMap& map, const Params& prm, int grid, cudaStream_t
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cuda_check(cudaLaunchKernelEx(&cfg, gemm_w4a8_tc<MT, PATH, GB1>, map, prm),
+  cuda_check(cudaLaunchKernelEx(&cfg, gemm_w4a8_tc<MT, PATH, GB1, XQ>, map, prm),
              "gemm_w4a8_tc launch");
   count_launch();
 }
@@ -653,23 +818,37 @@ int pick_mt(int64_t m) {
   return 128;
 }
 
-int cluster_capacity(int mt, int C) {
-  // Co-resident clusters per device; cached per (mt, C).
+int cluster_capacity(int mt, int C, bool xq) {
+  // Co-resident clusters per device; cached per (mt, C, fused).
   static std::mutex mu;
-  static int cache[4][9] = {};
+  static int cache[2][4][9] = {};
   const int mi = mt == 16 ? 0 : mt == 32 ? 1 : mt == 64 ? 2 : 3;
   std::lock_guard<std::mutex> lk(mu);
-  if (!cache[mi][C]) {
+  int& slot = cache[xq ? 1 : 0][mi][C];
+  if (!slot) {
     int n = 0;
-    switch (mt) {
-      case 16: n = max_active_clusters<16, ISB_PATH_INTEGER_SCALE, true>(C); break;
-      case 32: n = max_active_clusters<32, ISB_PATH_INTEGER_SCALE, true>(C); break;
-      case 64: n = max_active_clusters<64, ISB_PATH_INTEGER_SCALE, true>(C); break;
-      default: n = max_active_clusters<128, ISB_PATH_INTEGER_SCALE, true>(C); break;
+    if (xq) {
+      switch (mt) {
+        case 16: n = max_active_clusters<16, ISB_PATH_INTEGER_SCALE, true, true>(C); break;
+        case 32: n = max_active_clusters<32, ISB_PATH_INTEGER_SCALE, true, true>(C); break;
+        default: n = max_active_clusters<64, ISB_PATH_INTEGER_SCALE, true, true>(C); break;
+      }
+    } else {
+      switch (mt) {
+        case 16: n = max_active_clusters<16, ISB_PATH_INTEGER_SCALE, true, false>(C); break;
+        case 32: n = max_active_clusters<32, ISB_PATH_INTEGER_SCALE, true, false>(C); break;
+        case 64: n = max_active_clusters<64, ISB_PATH_INTEGER_SCALE, true, false>(C); break;
+        default: n = max_active_clusters<128, ISB_PATH_INTEGER_SCALE, true, false>(C); break;
+      }
     }
-    cache[mi][C] = n > 0 ? n : -1;
+    slot = n > 0 ? n : -1;
   }
-  return cache[mi][C];
+  return slot;
+}
+
+int xres_blocks(int mt) {
+  return mt == 16 ? Cfg<16, true>::kXResBlocks
+                  : mt == 32 ? Cfg<32, true>::kXResBlocks : Cfg<64, true>::kXResBlocks;
 }
 
 }  // namespace
@@ -705,46 +884,67 @@ CUtensorMap make_x_map(const int8_t* xq, int64_t m, int64_t k, int mt) {
 }
 
 
-GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path) {
+GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path, bool fused) {
   (void)path;
   GemmPlan pl;
   pl.mt = pick_mt(m);
   pl.m_tiles = static_cast<int>((m + pl.mt - 1) / pl.mt);
   pl.tiles = static_cast<int>(w.n_tiles) * pl.m_tiles;
   pl.units = static_cast<int64_t>(pl.tiles) * w.groups;
+  pl.fused = fused;
   // Choose the cluster size C (split-K ways): makespan ~ rounds * (steps per CTA
-  // + per-tile overhead), rounds = ceil(tiles / co-resident clusters).
+  // + per-tile overhead), rounds = ceil(tiles / co-resident clusters). Fused
+  // activation quantization also needs every rank's K slice to fit the resident
+  // budget.
   const int S = pl.mt <= 32 ? 4 : (pl.mt == 64 ? 2 : 1);
+  const int64_t gb = w.group / kBlockK;
   double best = 1e30;
-  pl.cluster = 1;
+  pl.cluster = 0;
   pl.grid = 1;
   for (int C : {1, 2, 4, 8}) {
     if (C > w.groups) break;
     if (C > 1 && pl.mt >= 128) break;  // two epilogue warpgroups: no cluster split-K
-    int cap = cluster_capacity(pl.mt, C);
+    const int64_t groups_cta = (w.groups + C - 1) / C;
+    if (fused && groups_cta * gb > xres_blocks(pl.mt)) continue;
+    int cap = cluster_capacity(pl.mt, C, fused);
     if (cap <= 0) continue;
     cap = std::min(cap, num_sms / C);
     const int nc = std::min(cap, pl.tiles);
     const int rounds = (pl.tiles + nc - 1) / nc;
-    const int64_t groups_cta = (w.groups + C - 1) / C;
-    const int64_t kb_cta = groups_cta * (w.group / kBlockK);
+    const int64_t kb_cta = groups_cta * gb;
     const double steps = std::ceil(static_cast<double>(kb_cta) / S);
     // ~2 steps of fixed cost per tile (pipeline fill/drain, reduction)
-    const double cost = rounds * (steps + 2.0 + (C > 1 ? 0.5 : 0.0));
+    double cost = rounds * (steps + 2.0 + (C > 1 ? 0.5 : 0.0));
+    // fused: every CTA first reads its float activation slice (4 B / element),
+    // counted in units of one step's 32 KiB of weights.
+    if (fused) cost += static_cast<double>(pl.mt) * kb_cta * kBlockK * 4.0 / (4.0 * kBlockBytes);
     if (cost < best - 1e-9) {
       best = cost;
       pl.cluster = C;
       pl.grid = nc * C;
     }
   }
+  if (pl.cluster == 0) {  // fused: no cluster size fits the resident slice
+    if (fused) fail(ISB_PARAM, "fused activation quantization: K slice too large");
+    pl.cluster = 1;
+  }
   pl.maxc = pl.cluster;
   pl.workspace_bytes = 0;  // split-K reduces through DSMEM: no global workspace
   return pl;
 }
 
+bool act_fused_eligible(int64_t m, int64_t k, const isb_weight& w) {
+  if (m < 1 || m > 64 || !w.tensor_core_ok() || k != w.k) return false;
+  const int mt = pick_mt(m);
+  const int64_t gb = w.group / kBlockK;
+  for (int C : {1, 2, 4, 8})
+    if (C <= w.groups && ((w.groups + C - 1) / C) * gb <= xres_blocks(mt)) return true;
+  return false;
+}
+
 void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                     void* out, int out_dtype, void* workspace, const GemmPlan& pl,
-                    cudaStream_t s) {
+                    cudaStream_t s, const void* xf, int x_dtype, double* sa_out) {
   (void)workspace;
   Params prm{};
   prm.packed = w.packed;
@@ -768,26 +968,39 @@ void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, con
   prm.dbg = g_dbg;
   prm.late_shift = (path == ISB_PATH_INTEGER_SCALE && w.static_bound > 0 &&
                     w.static_bound <= (int64_t{1} << 27) - 1) ? 1 : 0;
-  const CUtensorMap map = make_x_map(xq, m, w.k, pl.mt);
+  prm.xf = xf;
+  prm.x_dtype = x_dtype;
+  prm.K = static_cast<int>(w.k);
+  prm.sa_out = sa_out;
+  CUtensorMap map{};
+  if (!pl.fused) map = make_x_map(xq, m, w.k, pl.mt);
   const bool gb1 = prm.gb == 1;
-#define ISB_DISPATCH(MTV)                                                                   \
-  case MTV:                                                                                 \
-    if (path == ISB_PATH_INTEGER_SCALE) {                                                   \
-      if (gb1) launch_mt<MTV, ISB_PATH_INTEGER_SCALE, true>(map, prm, pl.grid, s);          \
-      else launch_mt<MTV, ISB_PATH_INTEGER_SCALE, false>(map, prm, pl.grid, s);             \
-    } else {                                                                                \
-      if (gb1) launch_mt<MTV, ISB_PATH_FLOAT_SCALE, true>(map, prm, pl.grid, s);            \
-      else launch_mt<MTV, ISB_PATH_FLOAT_SCALE, false>(map, prm, pl.grid, s);               \
-    }                                                                                       \
+#define ISB_DISPATCH_P(MTV, PV, XQV)                                          \
+  if (gb1) launch_mt<MTV, PV, true, XQV>(map, prm, pl.grid, s);               \
+  else launch_mt<MTV, PV, false, XQV>(map, prm, pl.grid, s);
+#define ISB_DISPATCH(MTV, XQV)                                                \
+  case MTV:                                                                   \
+    if (path == ISB_PATH_INTEGER_SCALE) { ISB_DISPATCH_P(MTV, ISB_PATH_INTEGER_SCALE, XQV) } \
+    else { ISB_DISPATCH_P(MTV, ISB_PATH_FLOAT_SCALE, XQV) }                   \
     break;
-  switch (pl.mt) {
-    ISB_DISPATCH(16)
-    ISB_DISPATCH(32)
-    ISB_DISPATCH(64)
-    ISB_DISPATCH(128)
-    default: fail(ISB_ERROR, "bad tile");
+  if (pl.fused) {
+    switch (pl.mt) {
+      ISB_DISPATCH(16, true)
+      ISB_DISPATCH(32, true)
+      ISB_DISPATCH(64, true)
+      default: fail(ISB_ERROR, "bad tile");
+    }
+  } else {
+    switch (pl.mt) {
+      ISB_DISPATCH(16, false)
+      ISB_DISPATCH(32, false)
+      ISB_DISPATCH(64, false)
+      ISB_DISPATCH(128, false)
+      default: fail(ISB_ERROR, "bad tile");
+    }
   }
 #undef ISB_DISPATCH
+#undef ISB_DISPATCH_P
 }
 
 }  // namespace isb

@@ -57,6 +57,14 @@ void launch_tile_scales(const int32_t* int_scales, const double* scales, int64_t
 void launch_unpack(const isb_weight& w, int16_t* codes, cudaStream_t s);
 void launch_repack_signed4(const isb_weight& w, uint8_t* bytes, cudaStream_t s);
 
+// Tensor-parallel helpers (tp.cu).
+void launch_row_absmax(const void* x, int x_dtype, int64_t m, int64_t k, float* amax,
+                       cudaStream_t s);
+void launch_quantize_amax(const void* x, int x_dtype, int64_t m, int64_t k, const float* amax,
+                          int8_t* codes, double* scales, cudaStream_t s);
+void launch_finalize_acc(const int32_t* acc, const double* sa, int64_t m, int64_t n,
+                         double inv_amp, void* out, int out_dtype, cudaStream_t s);
+
 struct GemmPlan {
   int mt = 0;         // tokens per tile (UMMA N)
   int m_tiles = 0;
@@ -66,11 +74,14 @@ struct GemmPlan {
   int maxc = 1;       // max CTAs contributing to one tile
   int cluster = 1;    // split-K ways (thread-block cluster size)
   int64_t workspace_bytes = 0;
+  bool fused = false; // per-token activation quantization fused into the GEMM (gemm_tc.cu XQ)
 };
 extern int64_t* g_trace;  // debug timeline buffer (8 x 512 int64), nullptr = off
 extern int g_trace_cta;
 extern int g_dbg;
-GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path);
+GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path, bool fused = false);
+// Fused act-quant GEMM (decode M <= 64) possible for this weight (resident K slice fits).
+bool act_fused_eligible(int64_t m, int64_t k, const isb_weight& w);
 // 2-D TMA map over int8 activations [m][k], box 128 (K) x mt (rows), SWIZZLE_128B.
 CUtensorMap make_x_map(const int8_t* xq, int64_t m, int64_t k, int mt);
 // Prefill K3 with k_g folded into the weight expansion (gemm_fold.cu).
@@ -87,7 +98,8 @@ void launch_gemm_decode(int path, const int8_t* xq, const double* sa, int64_t m,
                         int num_sms, cudaStream_t s);
 void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                     void* out, int out_dtype, void* workspace, const GemmPlan& plan,
-                    cudaStream_t s);
+                    cudaStream_t s, const void* xf = nullptr, int x_dtype = 0,
+                    double* sa_out = nullptr);
 void launch_gemm_checked(int path, const int8_t* xq, const double* sa, int64_t m,
                          const isb_weight& w, float* out, double* out_f64, int64_t* acc,
                          int64_t* partials, unsigned long long* stats_dev, cudaStream_t s);

@@ -11,6 +11,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "layout.cuh"
+#include "quant.cuh"
 
 #include <algorithm>
 
@@ -18,20 +19,6 @@ namespace isb {
 namespace {
 
 constexpr int kQuantThreads = 256;
-
-// llround(double(x) / s) with the division replaced by a multiply by the
-// reciprocal except within 1e-9 of a rounding tie, where the exact IEEE
-// quotient decides. |y - x/s| <= ~4e-14 for |x/s| <= 127, so outside that
-// window round(y) == llround(RN(x/s)).
-__device__ __forceinline__ int quant_one(float xf, double s, double r, int qmin, int qmax) {
-  const double x = static_cast<double>(xf);
-  const double y = x * r;
-  const double ay = fabs(y);
-  const double frac = ay - floor(ay);
-  double q = (fabs(frac - 0.5) > 1e-9) ? round(y) : round(x / s);
-  q = fmin(fmax(q, static_cast<double>(qmin)), static_cast<double>(qmax));
-  return static_cast<int>(q);
-}
 
 __device__ __forceinline__ float block_max(float v, float* red) {
 #pragma unroll
@@ -49,33 +36,6 @@ __device__ __forceinline__ float block_max(float v, float* red) {
   const float r = red[0];
   __syncthreads();
   return r;
-}
-
-template <typename T>
-__device__ __forceinline__ void load4(const T* p, float (&v)[4]);
-
-template <>
-__device__ __forceinline__ void load4<float>(const float* p, float (&v)[4]) {
-  const float4 f = __ldg(reinterpret_cast<const float4*>(p));
-  v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-}
-
-template <>
-__device__ __forceinline__ void load4<__nv_bfloat16>(const __nv_bfloat16* p, float (&v)[4]) {
-  const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
-  v[0] = __uint_as_float(u.x << 16);
-  v[1] = __uint_as_float(u.x & 0xFFFF0000u);
-  v[2] = __uint_as_float(u.y << 16);
-  v[3] = __uint_as_float(u.y & 0xFFFF0000u);
-}
-
-template <typename T>
-__device__ __forceinline__ float load1(const T* p);
-template <>
-__device__ __forceinline__ float load1<float>(const float* p) { return __ldg(p); }
-template <>
-__device__ __forceinline__ float load1<__nv_bfloat16>(const __nv_bfloat16* p) {
-  return __bfloat162float(*p);
 }
 
 // One CTA per token row; the row stays in registers (V x 4 elements per

@@ -13,10 +13,11 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (ISB_BF16, ISB_F16, ISB_F32, ISB_PATH_FLOAT_SCALE, ISB_PATH_INTEGER_SCALE,
-                   GemmStats, WeightInfo, check, load)
+from ._lib import (ISB_BF16, ISB_F16, ISB_F32, ISB_I32, ISB_PATH_FLOAT_SCALE,
+                   ISB_PATH_INTEGER_SCALE, GemmStats, WeightInfo, check, load)
 
-_DT = {torch.float32: ISB_F32, torch.bfloat16: ISB_BF16, torch.float16: ISB_F16}
+_DT = {torch.float32: ISB_F32, torch.bfloat16: ISB_BF16, torch.float16: ISB_F16,
+       torch.int32: ISB_I32}
 
 
 def _ptr(t):
@@ -55,6 +56,52 @@ def quantize_per_token(x: torch.Tensor, check_finite: bool = False, stream=None,
     check(load().isb_quantize_per_token(_ptr(x), _DT[x.dtype], m, k, _ptr(codes), _ptr(scales),
                                         int(check_finite), _stream(stream)))
     return codes, scales
+
+
+def row_absmax(x: torch.Tensor, stream=None) -> torch.Tensor:
+    """Per-row max|x| (float32 [M]) of a (local, K-sharded) activation slice — the
+    partial a row-parallel layer all-reduces with MAX before quantizing."""
+    x = _cuda(x)
+    if x.dtype not in (torch.float32, torch.bfloat16) or x.dim() != 2:
+        raise _lib.ParamError("activations must be 2-d float32 or bfloat16")
+    m, k = x.shape
+    amax = torch.empty((m,), dtype=torch.float32, device=x.device)
+    check(load().isb_row_absmax(_ptr(x), _DT[x.dtype], m, k, _ptr(amax), _stream(stream)))
+    return amax
+
+
+def quantize_per_token_amax(x: torch.Tensor, amax: torch.Tensor, codes=None, scales=None,
+                            stream=None):
+    """quantize(x, 8, symmetric, per_token) of a K-slice given the FULL-row absmax
+    (quantize.cpp:120-125): codes equal the slice of the full-row quantization."""
+    x = _cuda(x)
+    amax = _cuda(amax, torch.float32)
+    if x.dtype not in (torch.float32, torch.bfloat16) or x.dim() != 2:
+        raise _lib.ParamError("activations must be 2-d float32 or bfloat16")
+    m, k = x.shape
+    if amax.numel() != m:
+        raise _lib.DimensionError(f"amax has {amax.numel()} rows, activations {m}")
+    if codes is None:
+        codes = torch.empty((m, k), dtype=torch.int8, device=x.device)
+    if scales is None:
+        scales = torch.empty((m,), dtype=torch.float64, device=x.device)
+    check(load().isb_quantize_per_token_amax(_ptr(x), _DT[x.dtype], m, k, _ptr(amax),
+                                             _ptr(codes), _ptr(scales), _stream(stream)))
+    return codes, scales
+
+
+def finalize_acc(acc: torch.Tensor, sa: torch.Tensor, amplifier: int, out_dtype=torch.bfloat16,
+                 out=None, stream=None) -> torch.Tensor:
+    """Eq. 2 epilogue of an (all-reduced) int32 accumulator (gemm.cpp:252):
+    out = float((acc / amplifier) * s_a)."""
+    acc = _cuda(acc, torch.int32)
+    sa = _cuda(sa, torch.float64)
+    m, n = acc.shape
+    if out is None:
+        out = torch.empty((m, n), dtype=out_dtype, device=acc.device)
+    check(load().isb_finalize_acc(_ptr(acc), _ptr(sa), m, n, int(amplifier), _ptr(out),
+                                  _DT[out.dtype], _stream(stream)))
+    return out
 
 
 def quantize_weight(w: torch.Tensor, group: int = 128, bit_width: int = 4, stream=None):
@@ -241,7 +288,9 @@ def _gemm(path, xq, sa, w: PackedWeight, out_dtype, out, workspace, stream):
 
 def gemm_integer_scale(xq, sa, w: PackedWeight, out_dtype=torch.bfloat16, out=None,
                        workspace=None, stream=None):
-    """K3 — gemm_integer_scale (gemm.cpp:205-262) on tcgen05."""
+    """K3 — gemm_integer_scale (gemm.cpp:205-262) on tcgen05. out_dtype=torch.int32
+    returns the raw scaled accumulator sum_g P_g k_g (row-parallel TP; see
+    finalize_acc)."""
     return _gemm(ISB_PATH_INTEGER_SCALE, xq, sa, w, out_dtype, out, workspace, stream)
 
 
@@ -249,6 +298,27 @@ def gemm_float_scale(xq, sa, w: PackedWeight, out_dtype=torch.bfloat16, out=None
                      workspace=None, stream=None):
     """K4 — gemm_float_scale (gemm.cpp:156-203), fp32 I2F+FFMA per group, on tcgen05."""
     return _gemm(ISB_PATH_FLOAT_SCALE, xq, sa, w, out_dtype, out, workspace, stream)
+
+
+def gemm_act_fused(x, w: PackedWeight, path: str = "integer-scale", out_dtype=torch.bfloat16,
+                   out=None, sa_out=None, workspace=None, stream=None):
+    """K1 (+) K3/K4 in one launch (config C3): float32/bf16 activations in, the
+    same output as quantize_per_token + gemm_integer_scale / gemm_float_scale.
+    `sa_out` (float64 [M], optional) receives the per-token scales."""
+    x = _cuda(x)
+    if x.dtype not in (torch.float32, torch.bfloat16) or x.dim() != 2:
+        raise _lib.ParamError("activations must be 2-d float32 or bfloat16")
+    m, k = x.shape
+    if out is None:
+        out = torch.empty((m, w.n), dtype=out_dtype, device=x.device)
+    if sa_out is not None:
+        sa_out = _cuda(sa_out, torch.float64)
+    ws, need = _ws_for(m, w, workspace)
+    p = ISB_PATH_INTEGER_SCALE if path == "integer-scale" else ISB_PATH_FLOAT_SCALE
+    check(load().isb_gemm_act_fused(p, _ptr(x), _DT[x.dtype], m, k, w.handle, _ptr(out),
+                                    _DT[out.dtype], _ptr(sa_out), _ptr(ws), ws.numel(),
+                                    _stream(stream)))
+    return out
 
 
 def gemm_checked(path: str, xq, sa, w: PackedWeight, strict=False, want_f64=True, want_acc=True,

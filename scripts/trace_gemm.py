@@ -28,11 +28,19 @@ out = torch.empty((m, n), dtype=torch.bfloat16, device=dev)
 for i in range(4):
     isb.gemm_integer_scale(q, sa, ws[i % 3], out=out)
 torch.cuda.synchronize()
+xfl0 = torch.randn((m, k), device=dev)
+for i in range(3):
+    isb.gemm_act_fused(xfl0, ws[i % 3], out=out)
+torch.cuda.synchronize()
 tr = torch.zeros((32, 512), dtype=torch.int64, device=dev)
 lib = _lib.load()
 lib.isb_debug_set_trace.argtypes = [C.c_void_p, C.c_int]
 lib.isb_debug_set_trace(C.c_void_p(tr.data_ptr()), cta)
-isb.gemm_integer_scale(q, sa, ws[1], out=out)
+xfl = torch.randn((m, k), device=dev)
+if os.environ.get("FUSED"):
+    isb.gemm_act_fused(xfl, ws[1], out=out)
+else:
+    isb.gemm_integer_scale(q, sa, ws[1], out=out)
 torch.cuda.synchronize()
 lib.isb_debug_set_trace(None, 0)
 t = tr.cpu()
@@ -52,3 +60,5 @@ for it in range(8):
     vals = [int(t[r, it]) - mn if int(t[r, it]) else -1 for r in (8, 6, 7, 7)]
     if vals[0] > 0:
         print(f"tile {it}: epi_done={vals[0]} red_start={vals[1]} red_done={vals[2]}")
+
+print("fused prologue (ns): entry/pdl/pass1/exchange/pass2:", [int(t[9, i]) - mn if int(t[9, i]) else None for i in range(5)])

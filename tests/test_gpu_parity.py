@@ -319,3 +319,43 @@ def test_fold_extreme_codes_and_k16():
     out = isb.gemm_integer_scale(dev(x.values, torch.int8), dev(x.scales), pack(w, s),
                                  out_dtype=torch.float32).cpu().numpy()
     assert np.array_equal(out.view(np.int32), ref.output.view(np.int32))
+
+
+# ------------------------------------------------------------------------- K1 (+) K3 fused
+@pytest.mark.parametrize("m,k,n", [(1, 4096, 4096), (5, 4096, 12288), (16, 11008, 4096),
+                                   (16, 4096, 22016), (33, 2048, 640), (64, 4096, 1024),
+                                   (100, 1024, 256)])
+def test_act_fused_matches_quantize_then_gemm(m, k, n):
+    """Config C3: per-token quantization fused into the GEMM (one launch) gives the
+    reference codes/scales and the bit-exact integer-scale output; M = 100 takes the
+    unfused fallback."""
+    x, w, s, xf, _ = llama_problem(m, k, n, seed_w=23 + n, seed_x=29 + m)
+    ref = O.gemm_integer_scale(x, w, s)
+    pw = pack(w, s)
+    xd = dev(xf)
+    sa = torch.empty((m,), dtype=torch.float64, device=DEV)
+    out = isb.gemm_act_fused(xd, pw, out_dtype=torch.float32, sa_out=sa)
+    torch.cuda.synchronize()
+    assert np.array_equal(sa.cpu().numpy(), x.scales)
+    got = out.cpu().numpy()
+    assert np.array_equal(got.view(np.int32), ref.output.view(np.int32))
+    outf = isb.gemm_act_fused(xd, pw, path="float-scale", out_dtype=torch.float32)
+    rf = O.gemm_float_scale(x, w)
+    err = np.abs(outf.cpu().numpy().astype(np.float64) - rf.output_f64)
+    assert err.max() <= 1e-5 * np.abs(rf.output_f64).max() + 1e-30
+
+
+def test_act_fused_bf16_input_and_zero_rows():
+    m, k, n = 7, 4096, 512
+    x, w, s, xf, _ = llama_problem(m, k, n, seed_w=3, seed_x=4)
+    xf[2, :] = 0.0  # an all-zero token: scale 1.0, codes 0 (quantize.cpp:123)
+    xb = torch.from_numpy(xf).to(torch.bfloat16)
+    xo = O.quantize_per_token(xb.float().numpy())
+    ref = O.gemm_integer_scale(xo, w, s)
+    pw = pack(w, s)
+    sa = torch.empty((m,), dtype=torch.float64, device=DEV)
+    out = isb.gemm_act_fused(xb.to(DEV), pw, out_dtype=torch.float32, sa_out=sa)
+    torch.cuda.synchronize()
+    assert np.array_equal(sa.cpu().numpy(), xo.scales)
+    assert xo.scales[2] == 1.0
+    assert np.array_equal(out.cpu().numpy().view(np.int32), ref.output.view(np.int32))
