@@ -359,3 +359,34 @@ def test_act_fused_bf16_input_and_zero_rows():
     assert np.array_equal(sa.cpu().numpy(), xo.scales)
     assert xo.scales[2] == 1.0
     assert np.array_equal(out.cpu().numpy().view(np.int32), ref.output.view(np.int32))
+
+
+# ------------------------------------------------------------------------- runtime
+@pytest.mark.parametrize("fused", [False, True])
+def test_graphed_linears_match_direct_calls(fused):
+    from paper_2405_14597_b200.runtime import GraphedLinears
+    shapes = [(4096, 1024), (2048, 640)]
+    m = 16
+    ws, xs, refs = [], [], []
+    for i, (k, n) in enumerate(shapes):
+        x, w, s, xf, _ = llama_problem(m, k, n, seed_w=31 + i, seed_x=37 + i)
+        ws.append(pack(w, s))
+        xs.append(xf)
+        refs.append(O.gemm_integer_scale(x, w, s).output)
+    g = GraphedLinears(ws, m, out_dtype=torch.float32, fused=fused).capture()
+    for step in range(3):
+        for j, xf in enumerate(xs):
+            g.host_inputs[j].copy_(torch.from_numpy(xf * (1.0 + step)))
+        g.run()
+        g.synchronize()
+        for j, xf in enumerate(xs):
+            k, n = shapes[j]
+            x2 = O.quantize_per_token((xf * (1.0 + step)).astype(np.float32))
+            w2 = O.QuantizedTensor  # noqa: F841 (weights unchanged)
+            got = g.host_outputs[j].numpy()
+            if step == 0:
+                assert np.array_equal(got.view(np.int32), refs[j].view(np.int32))
+            else:
+                _, w, s, _, _ = llama_problem(m, k, n, seed_w=31 + j, seed_x=37 + j)
+                ref = O.gemm_integer_scale(x2, w, s).output
+                assert np.array_equal(got.view(np.int32), ref.view(np.int32))
