@@ -374,6 +374,13 @@ def run_ours(args, ws, rank, local):
                           "tops_int": round(ops / us_i / 1e6, 1),
                           "hbm_frac_int": round(byts / us_i / 1e3 / peak, 3)})
 
+    # ---- Mixtral-8x7B expert FFN (config C5): 8 experts on this GPU, T=16 decode
+    # tokens top-2 routed (32 expert rows, 4 per expert), per expert K1 + gate/up
+    # GEMM (4096 -> 2 x 14336) + SiLU*up + K1 + down GEMM (14336 -> 4096); graph.
+    moe_res = None
+    if not args.no_moe:
+        moe_res = moe_bench(isb, dev, args)
+
     result = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -416,8 +423,57 @@ def run_ours(args, ws, rank, local):
         "gpu_launches": args.steps * step.kernels_per_step,
         "clocks": clk.summary(),
         "sweep": sweep,
+        "mixtral_moe": moe_res,
     }
     return result
+
+
+def moe_bench(isb, dev, args, n_experts=8, tokens=16, k=4096, f=14336):
+    import torch
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(77)
+    rows = 2 * tokens // n_experts
+    experts, byts = [], 0
+    for _ in range(n_experts):
+        packs = []
+        for kk, nn in ((k, 2 * f), (f, k)):
+            wf = llama_like_weight(kk, nn, gen, dev)
+            codes, scales = isb.quantize_weight(wf, GROUP, 4)
+            del wf
+            si = isb.integerize_scales(scales.cpu().numpy(), ALPHA)
+            packs.append(isb.PackedWeight.from_codes(codes, GROUP, scales, si.int_scales, ALPHA))
+            byts += alg_bytes(rows, kk, nn)
+        experts.append(packs)
+    x = [torch.randn((rows, k), generator=gen, device=dev) for _ in range(n_experts)]
+    gu = [torch.empty((rows, 2 * f), dtype=torch.float32, device=dev) for _ in range(n_experts)]
+    y = [torch.empty((rows, k), dtype=torch.bfloat16, device=dev) for _ in range(n_experts)]
+    wsp = isb.Workspace()
+
+    def step(_i):
+        for e, (w13, w2) in enumerate(experts):
+            q, sa = isb.quantize_per_token(x[e])
+            isb.gemm_integer_scale(q, sa, w13, out=gu[e], workspace=wsp)
+            h = torch.nn.functional.silu(gu[e][:, :f]) * gu[e][:, f:]
+            hq, hs = isb.quantize_per_token(h)
+            isb.gemm_integer_scale(hq, hs, w2, out=y[e], workspace=wsp)
+
+    step(0)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            step(0)
+    torch.cuda.current_stream().wait_stream(s)
+    n = max(20, min(args.steps, 200))
+    ms = time_steps(lambda i: g.replay(), n, args.warmup, 1) / n
+    ops_ = n_experts * 2 * rows * (k * 2 * f + f * k)
+    peak, _ = load_peaks()
+    return {"config": f"Mixtral-8x7B expert FFN, {n_experts} experts on 1 GPU, {tokens} tokens "
+                      f"top-2 ({rows} rows/expert), K1+GEMM+SiLU+K1+GEMM per expert, CUDA graph",
+            "us_per_moe_layer": round(ms * 1e3, 2), "tops": round(ops_ / (ms * 1e-3) / 1e12, 2),
+            "alg_bytes": byts, "hbm_frac": round(byts / (ms * 1e-3) / 1e9 / peak, 3)}
 
 
 # ----------------------------------------------------------------------------- CPU legs
@@ -532,6 +588,7 @@ def main():
     ap.add_argument("--sweep", type=int, nargs="*", default=[1, 16, 64, 2048])
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-moe", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
