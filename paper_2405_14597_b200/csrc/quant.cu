@@ -14,6 +14,7 @@
 #include "quant.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace isb {
 namespace {
@@ -147,6 +148,58 @@ __global__ void __launch_bounds__(kQuantThreads)
   }
 }
 
+// Decode-sized M, K <= 1024 * 4 * V: one 1024-thread CTA per token row, every
+// thread holds V float4 of the row, so all loads of the row are in flight at once
+// and a single block reduction gives the row max (no cluster barriers).
+template <int V, typename T>
+__global__ void __launch_bounds__(1024)
+    quantize_rows_wide(const T* __restrict__ x, int64_t k, int8_t* __restrict__ codes,
+                       double* __restrict__ scales, int* __restrict__ bad) {
+  __shared__ float red[32];
+  const int64_t row = blockIdx.x;
+  const T* xr = x + row * k;
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();  // x may be produced by the preceding grid
+  float v[V][4];
+  float amax = 0.0f;
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int64_t e = (static_cast<int64_t>(i) * 1024 + threadIdx.x) * 4;
+    if (e < k) {
+      load4<T>(xr + e, v[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        finite = finite && isfinite(v[i][j]);
+        amax = fmaxf(amax, fabsf(v[i][j]));
+      }
+    }
+  }
+  if (!finite) atomicExch(bad, 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = amax;
+  __syncthreads();
+  amax = red[threadIdx.x & 31];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const double s = amax == 0.0f ? 1.0 : static_cast<double>(amax) / 127.0;
+  const double r = 1.0 / s;
+  if (threadIdx.x == 0) scales[row] = s;
+  int8_t* cr = codes + row * k;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int64_t e = (static_cast<int64_t>(i) * 1024 + threadIdx.x) * 4;
+    if (e < k) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        packed |= (static_cast<uint32_t>(quant_one(v[i][j], s, r, -128, 127)) & 0xFFu) << (8 * j);
+      *reinterpret_cast<uint32_t*>(cr + e) = packed;
+    }
+  }
+}
+
 // Any K / alignment: two passes over the row (the second hits L2).
 template <typename T>
 __global__ void __launch_bounds__(kQuantThreads)
@@ -217,6 +270,24 @@ void launch_rows(const T* x, int64_t m, int64_t k, int8_t* codes, double* scales
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e;
+  // Decode-sized M: one 1024-thread CTA per row holds the whole row (K <= 16384).
+  static const int k1_mode = [] {  // ISB_K1=cluster keeps the cluster variant (A/B)
+    const char* e = std::getenv("ISB_K1");
+    return (e && e[0] == 'c') ? 1 : 0;
+  }();
+  if (vec_ok && m < 148 && k1_mode == 0 && k <= 4096 * 4) {
+    cfg.blockDim = dim3(1024);
+    const int64_t vw = (k + 4095) / 4096;
+    if (vw <= 1)
+      e = cudaLaunchKernelEx(&cfg, quantize_rows_wide<1, T>, x, k, codes, scales, bad);
+    else if (vw <= 2)
+      e = cudaLaunchKernelEx(&cfg, quantize_rows_wide<2, T>, x, k, codes, scales, bad);
+    else
+      e = cudaLaunchKernelEx(&cfg, quantize_rows_wide<4, T>, x, k, codes, scales, bad);
+    cuda_check(e, "quantize_per_token launch");
+    count_launch();
+    return;
+  }
   // Decode-sized M: spread each row over a cluster of CTAs (<= 1024 elements each).
   const int64_t cpr = std::min<int64_t>(8, (k + 1023) / 1024);
   if (vec_ok && m < 148 && cpr > 1 && round_up((k + cpr - 1) / cpr, 4) <= 4096) {
