@@ -35,6 +35,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 
@@ -812,9 +813,13 @@ void launch_mt(const CUtensorMap& map, const Params& prm, int grid, cudaStream_t
 }
 
 int pick_mt(int64_t m) {
+  static const bool mt64 = [] {  // ISB_MT64=1: the single 64-token tile for 32 < M <= 64 (A/B)
+    const char* e = std::getenv("ISB_MT64");
+    return e && e[0] == '1';
+  }();
   if (m <= 16) return 16;
   if (m <= 32) return 32;
-  if (m <= 64) return 64;
+  if (m <= 64) return mt64 ? 64 : 32;  // two 32-token tiles: MT=64 spills its accumulators
   return 128;
 }
 
