@@ -941,6 +941,7 @@ GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path, bool f
 bool act_fused_eligible(int64_t m, int64_t k, const isb_weight& w) {
   if (m < 1 || m > 64 || !w.tensor_core_ok() || k != w.k) return false;
   const int mt = pick_mt(m);
+  if (mt < m) return false;  // the resident slice holds one token tile
   const int64_t gb = w.group / kBlockK;
   for (int C : {1, 2, 4, 8})
     if (C <= w.groups && ((w.groups + C - 1) / C) * gb <= xres_blocks(mt)) return true;
