@@ -906,9 +906,14 @@ GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path, bool f
   double best = 1e30;
   pl.cluster = 0;
   pl.grid = 1;
+  static const int force_c = [] {  // ISB_FORCE_C=<1|2|4|8>: A/B of the split-K width
+    const char* e = std::getenv("ISB_FORCE_C");
+    return e ? std::atoi(e) : 0;
+  }();
   for (int C : {1, 2, 4, 8}) {
     if (C > w.groups) break;
     if (C > 1 && pl.mt >= 128) break;  // two epilogue warpgroups: no cluster split-K
+    if (force_c && C != force_c) continue;
     const int64_t groups_cta = (w.groups + C - 1) / C;
     if (fused && groups_cta * gb > xres_blocks(pl.mt)) continue;
     int cap = cluster_capacity(pl.mt, C, fused);
