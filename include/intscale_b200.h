@@ -46,7 +46,9 @@ enum isb_status {
  * row-parallel (K-sharded) layer all-reduces exactly; see isb_finalize_acc. */
 enum isb_dtype { ISB_F32 = 0, ISB_BF16 = 1, ISB_F16 = 2, ISB_I32 = 3 };
 
-enum isb_path { ISB_PATH_FLOAT_SCALE = 0, ISB_PATH_INTEGER_SCALE = 1 };
+/* ISB_PATH_COARSE: per-channel W4A8 (gemm_coarse, gemm.hpp:97) — the paper's
+ * coarse-grained comparison; internal to isb_gemm_coarse. */
+enum isb_path { ISB_PATH_FLOAT_SCALE = 0, ISB_PATH_INTEGER_SCALE = 1, ISB_PATH_COARSE = 2 };
 
 const char* isb_last_error(void);
 int isb_version(void);
@@ -164,6 +166,16 @@ int isb_finalize_acc(const int32_t* acc, const double* sa, int64_t m, int64_t n,
 int isb_row_absmax(const void* x, int x_dtype, int64_t m, int64_t k, float* amax, void* stream);
 int isb_quantize_per_token_amax(const void* x, int x_dtype, int64_t m, int64_t k,
                                 const float* amax, int8_t* codes, double* scales, void* stream);
+
+/* --------------------------------------------------------------------------
+ * Coarse-grained (per-channel) W4A8 — replaces gemm_coarse (gemm.hpp:97,
+ * gemm.cpp:264-309): out[i,j] = float((double(sum_k x*w) * s_w[j]) * s_a[i]),
+ * bit-exact (exact int32 sum on the tensor core, the reference's double
+ * epilogue). The weight must be per-channel: packed with group = K.
+ */
+int isb_gemm_coarse(const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                    const isb_weight* w, void* out, int out_dtype, void* workspace,
+                    int64_t workspace_bytes, void* stream);
 
 /* --------------------------------------------------------------------------
  * Checked GEMM (CUDA cores, int64): the full reference semantics for any

@@ -259,6 +259,16 @@ def gemm_float_scale(x: QuantizedTensor, w: QuantizedTensor, strict=False, worke
     return GemmResult(out, _stats_dict(st), of, None, part)
 
 
+def gemm_coarse(x: QuantizedTensor, w: QuantizedTensor, workers=1) -> "GemmResult":
+    """gemm_coarse, gemm.cpp:264-309: per-channel weights only (:267-268);
+    out = float(double(acc) * s_w[j] * s_a[i]) — the same double expression, in the
+    same order, as the float-scale path with a single group per channel
+    (gemm.cpp:190-194), which this restatement therefore shares."""
+    if w.kind != PER_CHANNEL:
+        raise OracleError(PARAM, "coarse path requires per-channel weights")
+    return gemm_float_scale(x, w, workers=workers)
+
+
 def gemm_oracle(path: str, x: QuantizedTensor, w: QuantizedTensor, amplifier=1):
     m, k = x.values.shape
     kw, n = w.values.shape

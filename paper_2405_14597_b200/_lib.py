@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("ISB_LIB_PATH") or os.path.join(_HERE, "libintscale_b2
 ISB_OK, ISB_PARAM, ISB_DIMENSION, ISB_VALUE, ISB_OVERFLOW, ISB_LENGTH, ISB_FORMAT, ISB_ERROR, \
     ISB_CUDA = range(9)
 ISB_F32, ISB_BF16, ISB_F16, ISB_I32 = 0, 1, 2, 3
-ISB_PATH_FLOAT_SCALE, ISB_PATH_INTEGER_SCALE = 0, 1
+ISB_PATH_FLOAT_SCALE, ISB_PATH_INTEGER_SCALE, ISB_PATH_COARSE = 0, 1, 2
 
 
 class IntscaleError(Exception):
@@ -99,6 +99,7 @@ SIGNATURES = {
     "isb_search_amplifier_exponent": (_INT, [_VP, _I64, C.POINTER(_I32)]),
     "isb_integerize_scales": (_INT, [_VP, _I64, _I64, _VP, C.POINTER(_I32)]),
     "isb_finalize_acc": (_INT, [_VP, _VP, _I64, _I64, _I64, _VP, _INT, _VP]),
+    "isb_gemm_coarse": (_INT, [_VP, _VP, _I64, _I64, _VP, _VP, _INT, _VP, _I64, _VP]),
     "isb_gemm_act_fused": (_INT, [_INT, _VP, _INT, _I64, _I64, _VP, _VP, _INT, _VP, _VP, _I64,
                                   _VP]),
     "isb_row_absmax": (_INT, [_VP, _INT, _I64, _I64, _VP, _VP]),

@@ -379,6 +379,25 @@ int isb_gemm_float_scale(const int8_t* xq, const double* sa, int64_t m, int64_t 
   });
 }
 
+int isb_gemm_coarse(const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                    const isb_weight* w, void* out, int out_dtype, void* workspace,
+                    int64_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    require_gemm_args(xq, sa, m, k, w, out_dtype);
+    if (out_dtype == ISB_I32) fail(ISB_PARAM, "unsupported output dtype");
+    if (w->groups != 1)
+      fail(ISB_PARAM, "coarse path requires per-channel weights");  // gemm.cpp:268
+    if (!w->tensor_core_ok())
+      fail(ISB_PARAM, "tcgen05 path needs K % 128 == 0 (use isb_gemm_checked)");
+    if (m > std::numeric_limits<int>::max() || w->n > std::numeric_limits<int>::max())
+      fail(ISB_PARAM, "shape too large");
+    (void)workspace_bytes;
+    const GemmPlan pl = plan_gemm(m, *w, num_sms(), ISB_PATH_COARSE);
+    launch_gemm_tc(ISB_PATH_COARSE, xq, sa, m, *w, out, out_dtype, workspace, pl,
+                   as_stream(stream));
+  });
+}
+
 int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t k,
                        const isb_weight* w, void* out, int out_dtype, double* sa_out,
                        void* workspace, int64_t workspace_bytes, void* stream) {

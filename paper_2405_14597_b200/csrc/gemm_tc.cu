@@ -113,6 +113,7 @@ struct Params {
   int x_dtype;
   int K;
   double* sa_out;         // XQ: optional per-token scales out [M] (written by rank 0)
+  const double* wscale_d; // coarse path: per-channel weight scales s_w[N] (double)
 };
 
 // Debug timeline: trace[role * 512 + i] = globaltimer at event i of that role.
@@ -137,10 +138,13 @@ __device__ __forceinline__ void store_out(void* out, int dtype, int64_t idx, flo
 
 // Eq. 2 epilogue (integer) / Eq. 1 (float): one double conversion per output.
 template <int PATH>
-__device__ __forceinline__ float finish(int32_t iacc, float facc, double s_a, double inv_amp) {
+__device__ __forceinline__ float finish(int32_t iacc, float facc, double s_a, double inv_amp,
+                                        double s_w = 0.0) {
   double o;
   if (PATH == ISB_PATH_INTEGER_SCALE)
     o = __dmul_rn(static_cast<double>(iacc) * inv_amp, s_a);  // (acc / 2^e) * s_a, /2^e exact
+  else if (PATH == ISB_PATH_COARSE)  // gemm_coarse (gemm.cpp:293): (double(acc) * s_w[j]) * s_a
+    o = __dmul_rn(__dmul_rn(static_cast<double>(iacc), s_w), s_a);
   else
     o = __dmul_rn(static_cast<double>(facc), s_a);
   return __double2float_rn(o);
@@ -173,13 +177,14 @@ __device__ __forceinline__ void reduce_tile(const Params& p, uint32_t pb, const 
           v[i][q] = CC > 1 ? ld_shared_cluster_u32(mapa_shared(off, q)) : ld_shared_u32(off);
         }
       const int64_t n = static_cast<int64_t>(nt) * kTileN + rr;
+      const double s_w = (PATH == ISB_PATH_COARSE && n < p.N) ? p.wscale_d[n] : 0.0;
 #pragma unroll
       for (int i = 0; i < CH; ++i) {
         int32_t is = 0;
         float fs = 0.0f;
 #pragma unroll
         for (int q = 0; q < CC; ++q) {
-          if (PATH == ISB_PATH_INTEGER_SCALE) is += static_cast<int32_t>(v[i][q]);
+          if (PATH != ISB_PATH_FLOAT_SCALE) is += static_cast<int32_t>(v[i][q]);
           else fs += __uint_as_float(v[i][q]);
         }
         const int64_t m = static_cast<int64_t>(mt) * MT + lo + c0 + i;
@@ -187,7 +192,8 @@ __device__ __forceinline__ void reduce_tile(const Params& p, uint32_t pb, const 
           if (PATH == ISB_PATH_INTEGER_SCALE && p.out_dtype == ISB_I32)
             static_cast<int32_t*>(p.out)[m * p.N + n] = is;  // raw acc (row-parallel TP)
           else
-            store_out(p.out, p.out_dtype, m * p.N + n, finish<PATH>(is, fs, sav[i], p.inv_amp));
+            store_out(p.out, p.out_dtype, m * p.N + n,
+                      finish<PATH>(is, fs, sav[i], p.inv_amp, s_w));
         }
       }
     }
@@ -591,7 +597,7 @@ __global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
             float sg = 0.0f;
             if (g_last) {
               const uint32_t sraw = ld_shared_u32(sc_base + ((kb + i) / p.gb - ga) * (kTileN * 4));
-              kg = static_cast<int32_t>(sraw);
+              kg = PATH == ISB_PATH_COARSE ? 1 : static_cast<int32_t>(sraw);
               sg = __uint_as_float(sraw);
             }
             const uint32_t taddr =
@@ -619,7 +625,7 @@ __global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
                   gsum[cc + t] = d;
                 }
                 if (g_last) {
-                  if (PATH == ISB_PATH_INTEGER_SCALE) {
+                  if (PATH != ISB_PATH_FLOAT_SCALE) {
                     // Eq. 2: int32 scaled accumulation. With 16x headroom under the
                     // static bound the x16 of the nibble expansion is removed once at
                     // the end (one IMAD per value instead of SHF + IMAD).
@@ -640,7 +646,7 @@ __global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
           mbar_arrive(&sc_empty[stage]);
         }
       }
-      if (PATH == ISB_PATH_INTEGER_SCALE && late) {
+      if (PATH != ISB_PATH_FLOAT_SCALE && late) {
 #pragma unroll
         for (int t = 0; t < kCols; ++t) iacc[t] >>= 4;  // exact: 16 | acc16
       }
@@ -654,7 +660,7 @@ __global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
 #pragma unroll
         for (int t = 0; t < kCols; ++t)
           asm volatile("st.shared.u32 [%0], %1;" ::"r"(pb + ((c0 + t) * kTileN + r) * 4),
-                       "r"(PATH == ISB_PATH_INTEGER_SCALE ? static_cast<uint32_t>(iacc[t])
+                       "r"(PATH != ISB_PATH_FLOAT_SCALE ? static_cast<uint32_t>(iacc[t])
                                                           : __float_as_uint(facc[t]))
                        : "memory");
         __syncwarp();
@@ -667,6 +673,7 @@ __global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
         const double* sa_t = sa_s + (it & 1) * MT;
         const int64_t n = static_cast<int64_t>(nt) * kTileN + r;
         if (n < p.N) {
+          const double s_w = PATH == ISB_PATH_COARSE ? p.wscale_d[n] : 0.0;
 #pragma unroll
           for (int t = 0; t < kCols; ++t) {
             const int64_t m = static_cast<int64_t>(mt) * MT + c0 + t;
@@ -675,7 +682,7 @@ __global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
                 static_cast<int32_t*>(p.out)[m * p.N + n] = iacc[t];
               else
                 store_out(p.out, p.out_dtype, m * p.N + n,
-                          finish<PATH>(iacc[t], facc[t], sa_t[c0 + t], p.inv_amp));
+                          finish<PATH>(iacc[t], facc[t], sa_t[c0 + t], p.inv_amp, s_w));
             }
           }
         }
@@ -979,6 +986,12 @@ void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, con
   prm.dbg = g_dbg;
   prm.late_shift = (path == ISB_PATH_INTEGER_SCALE && w.static_bound > 0 &&
                     w.static_bound <= (int64_t{1} << 27) - 1) ? 1 : 0;
+  if (path == ISB_PATH_COARSE) {
+    // exact int32 sum of 16 * x * w over the whole K: |.| <= 16 * K * 127 * 8
+    if (16 * w.k * 127 * 8 > (int64_t{1} << 31) - 1) fail(ISB_PARAM, "coarse path: K too large");
+    prm.late_shift = 1;
+  }
+  prm.wscale_d = w.scales;
   prm.xf = xf;
   prm.x_dtype = x_dtype;
   prm.K = static_cast<int>(w.k);
@@ -994,7 +1007,19 @@ void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, con
     if (path == ISB_PATH_INTEGER_SCALE) { ISB_DISPATCH_P(MTV, ISB_PATH_INTEGER_SCALE, XQV) } \
     else { ISB_DISPATCH_P(MTV, ISB_PATH_FLOAT_SCALE, XQV) }                   \
     break;
-  if (pl.fused) {
+#define ISB_DISPATCH_COARSE(MTV)                                              \
+  case MTV:                                                                   \
+    launch_mt<MTV, ISB_PATH_COARSE, false, false>(map, prm, pl.grid, s);     \
+    break;
+  if (path == ISB_PATH_COARSE) {  // per-channel weights: one group spanning K
+    switch (pl.mt) {
+      ISB_DISPATCH_COARSE(16)
+      ISB_DISPATCH_COARSE(32)
+      ISB_DISPATCH_COARSE(64)
+      ISB_DISPATCH_COARSE(128)
+      default: fail(ISB_ERROR, "bad tile");
+    }
+  } else if (pl.fused) {
     switch (pl.mt) {
       ISB_DISPATCH(16, true)
       ISB_DISPATCH(32, true)
@@ -1012,6 +1037,7 @@ void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, con
   }
 #undef ISB_DISPATCH
 #undef ISB_DISPATCH_P
+#undef ISB_DISPATCH_COARSE
 }
 
 }  // namespace isb

@@ -300,6 +300,21 @@ def gemm_float_scale(xq, sa, w: PackedWeight, out_dtype=torch.bfloat16, out=None
     return _gemm(ISB_PATH_FLOAT_SCALE, xq, sa, w, out_dtype, out, workspace, stream)
 
 
+def gemm_coarse(xq, sa, w: PackedWeight, out_dtype=torch.bfloat16, out=None, workspace=None,
+                stream=None):
+    """gemm_coarse (gemm.hpp:97, gemm.cpp:264-309): per-channel W4A8 (w packed with
+    group = K), out = float((double(acc) * s_w[j]) * s_a[i]) — bit-exact."""
+    xq = _cuda(xq, torch.int8)
+    sa = _cuda(sa, torch.float64)
+    m, k = xq.shape
+    if out is None:
+        out = torch.empty((m, w.n), dtype=out_dtype, device=xq.device)
+    ws, _ = _ws_for(m, w, workspace)
+    check(load().isb_gemm_coarse(_ptr(xq), _ptr(sa), m, k, w.handle, _ptr(out), _DT[out.dtype],
+                                 _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
 def gemm_act_fused(x, w: PackedWeight, path: str = "integer-scale", out_dtype=torch.bfloat16,
                    out=None, sa_out=None, workspace=None, stream=None):
     """K1 (+) K3/K4 in one launch (config C3): float32/bf16 activations in, the

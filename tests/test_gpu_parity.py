@@ -390,3 +390,28 @@ def test_graphed_linears_match_direct_calls(fused):
                 _, w, s, _, _ = llama_problem(m, k, n, seed_w=31 + j, seed_x=37 + j)
                 ref = O.gemm_integer_scale(x2, w, s).output
                 assert np.array_equal(got.view(np.int32), ref.view(np.int32))
+
+
+# ------------------------------------------------------------------------- coarse (per-channel)
+@pytest.mark.parametrize("m,k,n", [(1, 4096, 4096), (16, 4096, 1024), (5, 11008, 256),
+                                   (100, 1024, 256), (300, 2048, 640)])
+def test_coarse_per_channel_bit_exact(m, k, n):
+    """gemm_coarse (gemm.cpp:264-309) on tcgen05: exact int32 sum over K, the
+    reference's double epilogue (double(acc) * s_w) * s_a -> float32 0 ULP."""
+    wf = O.generate_llama_like(k, n, 61 + n)
+    xf = O.generate_gaussian(m, k, 1.0, 67 + m)
+    w = O.quantize(wf, 4, O.SYMMETRIC, O.PER_CHANNEL, k)
+    x = O.quantize_per_token(xf)
+    ref = O.gemm_coarse(x, w)
+    pw = isb.PackedWeight.from_codes(dev(w.values), k, dev(w.scales))
+    xq, sa = dev(x.values, torch.int8), dev(x.scales)
+    out = isb.gemm_coarse(xq, sa, pw, out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(out.view(np.int32), ref.output.view(np.int32))
+    outb = isb.gemm_coarse(xq, sa, pw, out_dtype=torch.bfloat16).float().cpu().numpy()
+    assert np.array_equal(outb, to_bf16_np(ref.output))
+
+
+def test_coarse_rejects_grouped_weights():
+    x, w, s, _, _ = llama_problem(4, 1024, 256)
+    with pytest.raises(isb.ParamError):
+        isb.gemm_coarse(dev(x.values, torch.int8), dev(x.scales), pack(w, s))

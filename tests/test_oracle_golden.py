@@ -565,3 +565,23 @@ def test_acceptance_8_overflow_soundness():  # acceptance.cpp:432-504
     fb = O.run_layer(x, w, "integer-scale", s, fallback=True)
     assert fb.stats["fallback_applied"] and not rep["safe"]
     assert np.array_equal(fb.output, O.gemm_float_scale(x, w).output)
+
+
+def test_coarse_equals_integer_path_when_k_equals_alpha():
+    """test_gemm.cpp:137-166 ("integer scales equal to the amplifier reproduce coarse
+    exactly"): group-of-2 unit scales integerised at alpha in {1, 8, 1024} vs
+    per-channel unit scales through gemm_coarse — identical outputs."""
+    rng = O.Rng(17)
+    m, k, n, g = 3, 8, 4, 2
+    xq = (rng.below(255, m * k) - 127).astype(np.int16).reshape(m, k)
+    wq = (rng.below(16, k * n) - 8).astype(np.int16).reshape(k, n)
+    sa = 0.25 + rng.u01(m)
+    x = O.QuantizedTensor(xq, 8, O.SYMMETRIC, O.PER_TOKEN, 0, np.asarray(sa, np.float64),
+                          np.zeros(0, np.int32))
+    wg = O.QuantizedTensor(wq, 4, O.SYMMETRIC, O.GROUP, g, np.ones((k // g) * n), np.zeros(0, np.int32))
+    wc = O.QuantizedTensor(wq, 4, O.SYMMETRIC, O.PER_CHANNEL, k, np.ones(n), np.zeros(0, np.int32))
+    for amp in (1, 8, 1024):
+        s = O.integerize_scales(wg.scales, amp)
+        ri = O.gemm_integer_scale(x, wg, s).output
+        rc = O.gemm_coarse(x, wc).output
+        assert np.array_equal(ri.view(np.int32), rc.view(np.int32))
