@@ -190,6 +190,20 @@ def test_workspace_is_left_clean_and_results_repeat():
     assert int(ws.buf.view(torch.int32).abs().sum()) == 0  # split-K workspace left clean
 
 
+def test_fold_2sm_kernel_subprocess():
+    """The opt-in cta_group::2 prefill kernel (ISB_FOLD2=1): bit-exact on the fold tests."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ISB_FOLD2="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"),
+                        "-k", "fold and not subprocess"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 def test_decode_stream_k_kernel_subprocess():
     """The opt-in stream-K decode kernel (ISB_DECODE=1, read once per process):
     bit-exact int32 / float32 on every split pattern, workspace left clean."""
