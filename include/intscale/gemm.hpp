@@ -56,6 +56,10 @@ GemmResult gemm_float_scale(const QuantizedTensor& x, const QuantizedTensor& w,
 GemmResult gemm_integer_scale(const QuantizedTensor& x, const QuantizedTensor& w,
                               const IntegerScaleSet& int_scales, const GemmOptions& opt = {});
 
+/// Coarse-grained (per-channel) W4A8, gemm.hpp:97 / gemm.cpp:264-309.
+GemmResult gemm_coarse(const QuantizedTensor& x, const QuantizedTensor& w,
+                       const GemmOptions& opt = {});
+
 struct PathConfig {
   PathKind kind = PathKind::integer_scale;
   const IntegerScaleSet* int_scales = nullptr;

@@ -410,6 +410,39 @@ GemmResult gemm_integer_scale(const QuantizedTensor& x, const QuantizedTensor& w
   return res;
 }
 
+GemmResult gemm_coarse(const QuantizedTensor& x, const QuantizedTensor& w,
+                       const GemmOptions& opt) {  // gemm.cpp:264-309
+  validate_activation(x);
+  if (w.params.granularity.kind != GranKind::per_channel)
+    throw ParamError("coarse path requires per-channel weights");  // gemm.cpp:267-268
+  const Index g = validate_grouped_weight(x, w);
+  const double t0 = now_ms();
+  Operands o(x, w, g, nullptr, 1);
+  GemmResult res;
+  const bool strict = opt.overflow == OverflowMode::strict;
+  const bool tc = o.k % 128 == 0;
+  // One group per channel: the checked float path computes the same
+  // double(acc) * s_w[j] * s_a[i] (gemm.cpp:190-194 with a single group).
+  if (strict || opt.record_partials || opt.track_accumulator || !tc)
+    run_checked(ISB_PATH_FLOAT_SCALE, o, strict, opt.record_partials, res);
+  if (tc) {  // tcgen05: exact int32 sum over K, the reference's double epilogue
+    Dev out(static_cast<std::size_t>(o.m * o.n) * 4);
+    Dev ws(256);
+    check(isb_gemm_coarse(o.xq.as<std::int8_t>(), o.sa.as<double>(), o.m, o.k, o.w.h, out.p,
+                          ISB_F32, ws.p, 256, nullptr));
+    MatF y(o.m, o.n);
+    down(y.data(), out, static_cast<std::size_t>(o.m * o.n));
+    if (res.output.size() && !(res.output == y))
+      throw Error("tcgen05 coarse output disagrees with the exact int64 pass");
+    res.output = std::move(y);
+    res.stats.tensor_core = true;
+  }
+  res.stats.int_to_float_conversions = o.m * o.n;      // gemm.cpp:303
+  res.stats.integer_multiply_adds = o.m * o.n * o.k;   // gemm.cpp:304
+  res.stats.wall_ms = now_ms() - t0;
+  return res;
+}
+
 GemmResult run_layer(const QuantizedTensor& x, const QuantizedTensor& w, const PathConfig& path,
                      FallbackPolicy fallback, const GemmOptions& opt) {  // gemm.cpp:489-516
   switch (path.kind) {
@@ -430,6 +463,7 @@ GemmResult run_layer(const QuantizedTensor& x, const QuantizedTensor& w, const P
       }
       return gemm_integer_scale(x, w, *path.int_scales, opt);
     }
+    case PathKind::coarse: return gemm_coarse(x, w, opt);
     default:
       throw ParamError("path '" + to_string(path.kind) + "' is outside the B200 integer-scale path");
   }

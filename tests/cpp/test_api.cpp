@@ -261,6 +261,53 @@ static void test_dyadic_agreement() {
 }
 
 // A LLaMA-shaped layer goes through tcgen05 and matches the exact int64 pass.
+static void test_coarse_equals_integer_at_alpha() {  // test_gemm.cpp:137-166
+  std::mt19937_64 rng(17);
+  auto u01 = [&] { return (rng() >> 11) * 0x1.0p-53; };
+  const Index m = 3, k = 8, n = 4, g = 2;
+  QuantizedTensor x;
+  x.values.resize(m, k);
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < k; ++j) x.values(i, j) = static_cast<std::int16_t>(rng() % 255) - 127;
+  QuantizedTensor wg;
+  wg.values.resize(k, n);
+  for (Index i = 0; i < k; ++i)
+    for (Index j = 0; j < n; ++j) wg.values(i, j) = static_cast<std::int16_t>(rng() % 16) - 8;
+  x.params.bit_width = 8;
+  x.params.scheme = Scheme::symmetric;
+  x.params.granularity = Granularity::per_token();
+  x.params.scales.resize(m);
+  for (Index i = 0; i < m; ++i) x.params.scales[i] = 0.25 + u01();
+  wg.params.bit_width = 4;
+  wg.params.scheme = Scheme::symmetric;
+  wg.params.granularity = Granularity::group_of(g);
+  wg.params.scales = VecD::Constant((k / g) * n, 1.0);
+  QuantizedTensor wc = wg;
+  wc.params.granularity = Granularity::per_channel();
+  wc.params.scales = VecD::Constant(n, 1.0);
+  for (std::int64_t amp : {1, 8, 1024}) {
+    auto set = integerize_scales(wg.params.scales, amp);
+    auto ri = gemm_integer_scale(x, wg, set);
+    auto rc = gemm_coarse(x, wc);
+    CHECK(ri.output == rc.output);
+  }
+  CHECK_THROWS_AS(gemm_coarse(x, wg), ParamError);  // gemm.cpp:267-268
+}
+
+static void test_coarse_tensor_core() {
+  std::mt19937_64 rng(5);
+  auto u01 = [&] { return (rng() >> 11) * 0x1.0p-53; };
+  const Index m = 7, k = 1024, n = 256;
+  MatF wf(k, n), xf(m, k);
+  for (Index i = 0; i < k * n; ++i) wf.data()[i] = static_cast<float>((2.0 * u01() - 1.0) * 0.01);
+  for (Index i = 0; i < m * k; ++i) xf.data()[i] = static_cast<float>(4.0 * u01() - 2.0);
+  auto w = quantize(wf, 4, Scheme::symmetric, Granularity::per_channel());
+  auto x = quantize(xf, 8, Scheme::symmetric, Granularity::per_token());
+  auto r = gemm_coarse(x, w);  // throws if the tcgen05 and exact outputs differ
+  CHECK(r.stats.tensor_core);
+  CHECK(r.stats.int_to_float_conversions == m * n);
+}
+
 static void test_tensor_core_layer() {
   std::mt19937_64 rng(42);
   auto u01 = [&] { return (rng() >> 11) * 0x1.0p-53; };
@@ -299,6 +346,8 @@ int main() {
       {"overflow_bound_pins", test_overflow_bound_pins},
       {"dyadic_agreement", test_dyadic_agreement},
       {"tensor_core_layer", test_tensor_core_layer},
+      {"coarse_equals_integer_at_alpha", test_coarse_equals_integer_at_alpha},
+      {"coarse_tensor_core", test_coarse_tensor_core},
   };
   for (const auto& [name, fn] : tests) {
     const int before = g_fail;
