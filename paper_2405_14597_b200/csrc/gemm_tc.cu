@@ -165,17 +165,21 @@ __device__ __forceinline__ void reduce_tile(const Params& p, uint32_t pb, const 
     double sav[CH];
 #pragma unroll
     for (int i = 0; i < CH; ++i) sav[i] = sa_t[lo + c0 + i];
+    // both row halves' partial loads in flight before first use: one DSMEM round trip
+    uint32_t vv[2][CH][CC];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint32_t rr = u + h * 64;
-      uint32_t v[CH][CC];
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int i = 0; i < CH; ++i)
 #pragma unroll
         for (int q = 0; q < CC; ++q) {
-          const uint32_t off = pb + ((lo + c0 + i) * kTileN + rr) * 4;
-          v[i][q] = CC > 1 ? ld_shared_cluster_u32(mapa_shared(off, q)) : ld_shared_u32(off);
+          const uint32_t off = pb + ((lo + c0 + i) * kTileN + u + h * 64) * 4;
+          vv[h][i][q] = CC > 1 ? ld_shared_cluster_u32(mapa_shared(off, q)) : ld_shared_u32(off);
         }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t rr = u + h * 64;
+      const uint32_t (&v)[CH][CC] = vv[h];
       const int64_t n = static_cast<int64_t>(nt) * kTileN + rr;
       const double s_w = (PATH == ISB_PATH_COARSE && n < p.N) ? p.wscale_d[n] : 0.0;
 #pragma unroll
