@@ -5,6 +5,9 @@
 // (ParamError).
 #pragma once
 
+#include <filesystem>
+#include <string>
+
 #include "intscale/types.hpp"
 
 namespace intscale {
@@ -45,5 +48,14 @@ struct QuantizedTensor {
 };
 
 QuantizedTensor quantize(const MatF& x, int bit_width, Scheme scheme, const Granularity& g);
+
+// Names and sidecar persistence (quantize.hpp:40-43, :91-93; quantize.cpp:56-82,
+// :175-270). The values go to a QTNS file, the parameters to `<path>.json`.
+std::string to_string(Scheme s);
+std::string to_string(GranKind k);
+Scheme scheme_from_string(const std::string& s);
+GranKind gran_kind_from_string(const std::string& s);
+void write_quantized(const QuantizedTensor& q, const std::filesystem::path& values_path);
+QuantizedTensor read_quantized(const std::filesystem::path& values_path);
 
 }  // namespace intscale

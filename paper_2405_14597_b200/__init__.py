@@ -14,6 +14,6 @@ from .ops import (IntegerScaleSet, PackedWeight, Workspace, finalize_acc,  # noq
                   quantize_per_token_amax, quantize_weight, row_absmax, search_amplifier,
                   search_amplifier_exponent, workspace_size)
 
-from . import moe, parallel, runtime  # noqa: F401,E402
+from . import moe, parallel, qtns, runtime  # noqa: F401,E402
 
 __version__ = "0.1.0"

@@ -7,9 +7,13 @@
 #include <intscale/quantize.hpp>
 #include <intscale/tensor_io.hpp>
 
+#include <unistd.h>
+
 #include <bit>
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
+#include <fstream>
 #include <functional>
 #include <random>
 #include <string>
@@ -334,6 +338,187 @@ static void test_tensor_core_layer() {
   CHECK(r2.stats.max_abs_accumulator == -1);
 }
 
+
+// ------------------------------------------------------------------ QTNS container
+namespace fs = std::filesystem;
+
+struct TempDir {  // test_tensor_io.cpp:21-33
+  fs::path path;
+  explicit TempDir(const std::string& tag) {
+    path = fs::temp_directory_path() / ("isb_io_" + tag + "_" + std::to_string(::getpid()));
+    fs::create_directories(path);
+  }
+  ~TempDir() {
+    std::error_code ec;
+    fs::remove_all(path, ec);
+  }
+  std::string file(const std::string& name) const { return (path / name).string(); }
+};
+
+static std::vector<std::uint8_t> slurp(const std::string& p) {
+  std::ifstream in(p, std::ios::binary);
+  return std::vector<std::uint8_t>(std::istreambuf_iterator<char>(in), {});
+}
+
+static void spit(const std::string& p, const std::vector<std::uint8_t>& b) {
+  std::ofstream out(p, std::ios::binary);
+  out.write(reinterpret_cast<const char*>(b.data()), static_cast<std::streamsize>(b.size()));
+}
+
+static std::vector<std::uint8_t> header_bytes(std::uint8_t dtype, std::uint64_t rows,
+                                              std::uint64_t cols) {
+  std::vector<std::uint8_t> h = {'Q', 'T', 'N', 'S', 1, 0, dtype, 2};
+  for (std::uint64_t d : {rows, cols})
+    for (int b = 0; b < 8; ++b) h.push_back(static_cast<std::uint8_t>((d >> (8 * b)) & 0xff));
+  return h;
+}
+
+static MatQ rowq(std::initializer_list<int> vals) {
+  MatQ m(1, static_cast<Index>(vals.size()));
+  Index j = 0;
+  for (int v : vals) m(0, j++) = static_cast<std::int16_t>(v);
+  return m;
+}
+
+static void test_qtns_containers() {  // test_tensor_io.cpp:88-161
+  TempDir tmp("hdr");
+  MatF z(1, 1);
+  write_tensor(z, tmp.file("z.qtns"));
+  auto expect = header_bytes(0, 1, 1);
+  expect.insert(expect.end(), {0, 0, 0, 0});
+  CHECK(slurp(tmp.file("z.qtns")) == expect);
+
+  MatF x(2, 3);
+  const float xv[] = {0.0f, -1.5f, 3.25e-3f, 1.0e30f, -1.0e-30f, 127.0f};
+  for (int i = 0; i < 6; ++i) x.data()[i] = xv[i];
+  write_tensor(x, tmp.file("x.qtns"));
+  CHECK(read_float_tensor(tmp.file("x.qtns")) == x);
+
+  MatQ q(2, 2);
+  q(0, 0) = -128, q(0, 1) = 127, q(1, 0) = 0, q(1, 1) = -1;
+  write_tensor(q, DType::signed8, tmp.file("q.qtns"));
+  auto d8 = read_tensor(tmp.file("q.qtns"));
+  auto* p8 = std::get_if<QuantizedPayload>(&d8);
+  CHECK(p8 && p8->bit_width == 8 && p8->values == q);
+
+  MatQ q4 = rowq({-8, 7, -1});
+  write_tensor(q4, DType::packed_signed4, tmp.file("q4.qtns"));
+  auto d4 = read_tensor(tmp.file("q4.qtns"));
+  auto* p4 = std::get_if<QuantizedPayload>(&d4);
+  CHECK(p4 && p4->bit_width == 4 && p4->values == q4);
+  CHECK(fs::file_size(tmp.file("q4.qtns")) == 26);
+
+  std::vector<std::uint8_t> v = {'Q', 'T', 'N', 'S', 1, 0, 1, 1, 5, 0, 0, 0, 0, 0, 0, 0,
+                                 0x80, 0xff, 0x00, 0x01, 0x7f};
+  spit(tmp.file("v.qtns"), v);
+  auto dv = read_tensor(tmp.file("v.qtns"));
+  auto* pv = std::get_if<QuantizedPayload>(&dv);
+  CHECK(pv && pv->values.rows() == 1 && pv->values.cols() == 5);
+  CHECK(pv && pv->values(0, 0) == -128 && pv->values(0, 1) == -1 && pv->values(0, 4) == 127);
+}
+
+static void test_qtns_malformed() {  // test_tensor_io.cpp:163-226
+  TempDir tmp("bad");
+  auto good = header_bytes(0, 1, 1);
+  good.insert(good.end(), {0, 0, 0, 0});
+  const std::string f = tmp.file("bad.qtns");
+  auto with = [&](std::size_t i, std::uint8_t val) {
+    auto b = good;
+    b[i] = val;
+    spit(f, b);
+  };
+  with(0, 'X');
+  CHECK_THROWS_AS(read_tensor(f), FormatError);
+  with(4, 2);
+  CHECK_THROWS_AS(read_tensor(f), FormatError);
+  with(6, 3);
+  CHECK_THROWS_AS(read_tensor(f), FormatError);
+  with(7, 3);
+  CHECK_THROWS_AS(read_tensor(f), FormatError);
+  spit(f, header_bytes(0, 0, 1));
+  CHECK_THROWS_AS(read_tensor(f), FormatError);
+  spit(f, std::vector<std::uint8_t>(good.begin(), good.end() - 1));
+  CHECK_THROWS_AS(read_tensor(f), LengthError);
+  spit(f, std::vector<std::uint8_t>(good.begin(), good.begin() + 10));
+  CHECK_THROWS_AS(read_tensor(f), FormatError);
+  auto trailing = good;
+  trailing.push_back(0);
+  spit(f, trailing);
+  CHECK_THROWS_AS(read_tensor(f), LengthError);
+  auto nan = header_bytes(0, 1, 1);
+  nan.insert(nan.end(), {0x00, 0x00, 0xc0, 0x7f});
+  spit(f, nan);
+  CHECK_THROWS_AS(read_tensor(f), ValueError);
+  CHECK_THROWS_AS(read_tensor(tmp.file("absent.qtns")), IoError);
+
+  MatF xn(1, 1);
+  xn(0, 0) = std::numeric_limits<float>::quiet_NaN();
+  CHECK_THROWS_AS(write_tensor(xn, tmp.file("nan.qtns")), ValueError);
+  MatQ big(1, 1);
+  big(0, 0) = 200;
+  CHECK_THROWS_AS(write_tensor(big, DType::signed8, tmp.file("big.qtns")), ValueError);
+  big(0, 0) = 8;
+  CHECK_THROWS_AS(write_tensor(big, DType::packed_signed4, tmp.file("big4.qtns")), ValueError);
+  big(0, 0) = 1;
+  CHECK_THROWS_AS(write_tensor(big, DType::real32, tmp.file("real.qtns")), ParamError);
+}
+
+static void test_quantized_sidecars() {  // test_quantize.cpp:284-328
+  TempDir tmp("persist");
+  std::mt19937_64 rng(9);
+  auto u01 = [&] { return (rng() >> 11) * 0x1.0p-53; };
+  MatF x(128, 4);
+  for (Index i = 0; i < x.rows(); ++i)
+    for (Index j = 0; j < x.cols(); ++j) x(i, j) = static_cast<float>(2.0 * u01() - 1.0);
+
+  auto q = quantize(x, 4, Scheme::symmetric, Granularity::group_of(32));
+  write_quantized(q, tmp.file("w.qtns"));
+  CHECK(fs::exists(tmp.file("w.qtns") + ".json"));
+  CHECK(fs::file_size(tmp.file("w.qtns")) == 24 + 256);
+  auto back = read_quantized(tmp.file("w.qtns"));
+  CHECK(back.values == q.values);
+  CHECK(back.params.bit_width == 4);
+  CHECK(back.params.scheme == Scheme::symmetric);
+  CHECK(back.params.granularity.kind == GranKind::group);
+  CHECK(back.params.granularity.group_size == 32);
+  CHECK(back.params.scales == q.params.scales);
+
+  // asymmetric codes (built by hand: the B200 quantizer is symmetric-only) survive
+  // the signed container through the fold / unfold
+  for (int bits : {4, 8}) {
+    QuantizedTensor a;
+    a.values.resize(3, 5);
+    for (Index i = 0; i < a.values.size(); ++i)
+      a.values.data()[i] = static_cast<std::int16_t>((i * 7) % (1 << bits));
+    a.params.bit_width = bits;
+    a.params.scheme = Scheme::asymmetric;
+    a.params.granularity = Granularity::per_token();
+    a.params.scales = VecD{0.5, 0.25, 1e-3};
+    a.params.zero_points = VecI{1, 2, 3};
+    write_quantized(a, tmp.file("a.qtns"));
+    auto ab = read_quantized(tmp.file("a.qtns"));
+    CHECK(ab.values == a.values);
+    CHECK(ab.params.zero_points == a.params.zero_points);
+    CHECK(ab.params.scales == a.params.scales);
+  }
+
+  const std::string side = tmp.file("w.qtns") + ".json";
+  auto put = [&](const std::string& s) { spit(side, std::vector<std::uint8_t>(s.begin(), s.end())); };
+  put("{not json");
+  CHECK_THROWS_AS(read_quantized(tmp.file("w.qtns")), FormatError);
+  put(R"({"bit_width": 8, "scheme": "symmetric", "granularity": {"kind": "group", "group_size": 32},
+          "scales": [], "zero_points": []})");
+  CHECK_THROWS_AS(read_quantized(tmp.file("w.qtns")), FormatError);
+  put(R"({"bit_width": 4, "scheme": "skewed", "granularity": {"kind": "group", "group_size": 32},
+          "scales": [], "zero_points": []})");
+  CHECK_THROWS_AS(read_quantized(tmp.file("w.qtns")), ParamError);
+  put(R"({"bit_width": 4, "scheme": "symmetric", "granularity": {"kind": "group", "group_size": 32},
+          "scales": [1.0], "zero_points": []})");
+  CHECK_THROWS_AS(read_quantized(tmp.file("w.qtns")), FormatError);
+  fs::remove(side);
+  CHECK_THROWS_AS(read_quantized(tmp.file("w.qtns")), IoError);
+}
+
 int main() {
   const std::pair<const char*, std::function<void()>> tests[] = {
       {"scalar_hand_example", test_scalar_hand_example},
@@ -348,6 +533,9 @@ int main() {
       {"tensor_core_layer", test_tensor_core_layer},
       {"coarse_equals_integer_at_alpha", test_coarse_equals_integer_at_alpha},
       {"coarse_tensor_core", test_coarse_tensor_core},
+      {"qtns_containers", test_qtns_containers},
+      {"qtns_malformed", test_qtns_malformed},
+      {"quantized_sidecars", test_quantized_sidecars},
   };
   for (const auto& [name, fn] : tests) {
     const int before = g_fail;
