@@ -157,14 +157,16 @@ __device__ __forceinline__ float finish(int32_t iacc, float facc, double s_a, do
 template <int MT, int CC, int PATH>
 __device__ __forceinline__ void reduce_tile(const Params& p, uint32_t pb, const double* sa_t,
                                             int rank, int nt, int mt, uint32_t u) {
-  constexpr int SL = MT / CC;
-  constexpr int CH = SL < 8 ? SL : 8;
-  const int lo = rank * SL;
+  // Rank `rank` finalises tokens [rank*MT/CC, (rank+1)*MT/CC) (uneven when CC = 3).
+  constexpr int SLM = (MT + CC - 1) / CC;
+  constexpr int CH = SLM < 8 ? SLM : 8;
+  const int lo = rank * MT / CC;
+  const int sl = (MT % CC == 0) ? MT / CC : (rank + 1) * MT / CC - lo;
 #pragma unroll 1
-  for (int c0 = 0; c0 < SL; c0 += CH) {
+  for (int c0 = 0; c0 < sl; c0 += CH) {
     double sav[CH];
 #pragma unroll
-    for (int i = 0; i < CH; ++i) sav[i] = sa_t[lo + c0 + i];
+    for (int i = 0; i < CH; ++i) sav[i] = (c0 + i < sl) ? sa_t[lo + c0 + i] : 0.0;
     // both row halves' partial loads in flight before first use: one DSMEM round trip
     uint32_t vv[2][CH][CC];
 #pragma unroll
@@ -173,7 +175,7 @@ __device__ __forceinline__ void reduce_tile(const Params& p, uint32_t pb, const 
       for (int i = 0; i < CH; ++i)
 #pragma unroll
         for (int q = 0; q < CC; ++q) {
-          const uint32_t off = pb + ((lo + c0 + i) * kTileN + u + h * 64) * 4;
+          const uint32_t off = pb + ((lo + min(c0 + i, sl - 1)) * kTileN + u + h * 64) * 4;
           vv[h][i][q] = CC > 1 ? ld_shared_cluster_u32(mapa_shared(off, q)) : ld_shared_u32(off);
         }
 #pragma unroll
@@ -192,7 +194,7 @@ __device__ __forceinline__ void reduce_tile(const Params& p, uint32_t pb, const 
           else fs += __uint_as_float(v[i][q]);
         }
         const int64_t m = static_cast<int64_t>(mt) * MT + lo + c0 + i;
-        if (n < p.N && m < p.M) {
+        if (c0 + i < sl && n < p.N && m < p.M) {
           if (PATH == ISB_PATH_INTEGER_SCALE && p.out_dtype == ISB_I32)
             static_cast<int32_t*>(p.out)[m * p.N + n] = is;  // raw acc (row-parallel TP)
           else
@@ -738,6 +740,7 @@ __global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
         switch (p.C) {
           case 1: reduce_tile<MT, 1, PATH>(p, pb, sa_t, wk.rank, nt, mt, u); break;
           case 2: reduce_tile<MT, 2, PATH>(p, pb, sa_t, wk.rank, nt, mt, u); break;
+          case 3: reduce_tile<MT, 3, PATH>(p, pb, sa_t, wk.rank, nt, mt, u); break;
           case 4: reduce_tile<MT, 4, PATH>(p, pb, sa_t, wk.rank, nt, mt, u); break;
           default: reduce_tile<MT, 8, PATH>(p, pb, sa_t, wk.rank, nt, mt, u); break;
         }
@@ -921,8 +924,9 @@ GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path, bool f
     const char* e = std::getenv("ISB_FORCE_C");
     return e ? std::atoi(e) : 0;
   }();
-  for (int C : {1, 2, 4, 8}) {
+  for (int C : {1, 2, 3, 4, 8}) {
     if (C > w.groups) break;
+    if (C == 3 && (fused || force_c != 3)) continue;  // C = 3 (uneven token split): opt-in
     if (C > 1 && pl.mt >= 128) break;  // two epilogue warpgroups: no cluster split-K
     if (force_c && C != force_c) continue;
     const int64_t groups_cta = (w.groups + C - 1) / C;
@@ -934,8 +938,11 @@ GemmPlan plan_gemm(int64_t m, const isb_weight& w, int num_sms, int path, bool f
     const int rounds = (pl.tiles + nc - 1) / nc;
     const int64_t kb_cta = groups_cta * gb;
     const double steps = std::ceil(static_cast<double>(kb_cta) / S);
-    // ~2 steps of fixed cost per tile (pipeline fill/drain, reduction)
-    double cost = rounds * (steps + 2.0 + (C > 1 ? 0.5 : 0.0));
+    // Per-tile cost beyond streaming: ~half a step (the next tile's loads are already
+    // in flight), plus the cluster reduction. Fitted on the LLaMA-2-7B decode shapes
+    // (profiles/r01_decode_planner.txt): a grid that leaves SMs idle (few tiles, C=1)
+    // loses to more rounds of a wider split.
+    double cost = rounds * (steps + 0.5 + (C > 1 ? 0.25 : 0.0));
     // fused: every CTA first reads its float activation slice (4 B / element),
     // counted in units of one step's 32 KiB of weights.
     if (fused) cost += static_cast<double>(pl.mt) * kb_cta * kBlockK * 4.0 / (4.0 * kBlockBytes);
