@@ -276,6 +276,37 @@ def gemm_kernel_timing(isb, layers, xq_sa, m, path, iters=30):
     return res
 
 
+def dense_layer_timing(isb, m, dev, wd, iters=10):
+    """Per-linear device time of the dense fp16 baseline (isb_gemm_dense, tcgen05
+    kind::f16, no cuBLAS) on the same shapes: fp16 x [M][K], fp16 w [N][K] rotated over
+    the replicas `wd`, CUDA graph, CUDA events."""
+    import torch
+    res = []
+    for i, (name, k, n) in enumerate(LAYER):
+        x = torch.randn((m, k), device=dev).half()
+        out = torch.empty((m, n), dtype=torch.float16, device=dev)
+        for r in range(len(wd)):
+            isb.gemm_dense(x, wd[r][i], out=out)
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for it in range(iters):
+                    isb.gemm_dense(x, wd[it % len(wd)][i], out=out)
+        torch.cuda.current_stream().wait_stream(s)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        res.append(e0.elapsed_time(e1) * 1000.0 / iters)
+    return res
+
+
 def run_ours(args, ws, rank, local):
     import numpy as np
     import torch
@@ -356,7 +387,12 @@ def run_ours(args, ws, rank, local):
         except Exception:
             traffic = None
 
-    # ---- prefill / decode sweep of the whole layer (kernel-only, int vs float)
+    # ---- dense fp16 baseline (hand-written tcgen05 kind::f16, no cuBLAS), same shapes
+    wd = [[(torch.randn((n, k), device=dev) * 0.02).half() for _, k, n in LAYER]
+          for _ in range(REPLICAS)]
+    dense_m = dense_layer_timing(isb, m, dev, wd, iters=30)
+
+    # ---- prefill / decode sweep of the whole layer (kernel-only, int vs float vs fp16)
     sweep = []
     if not args.no_sweep:
         for mm in args.sweep:
@@ -366,11 +402,14 @@ def run_ours(args, ws, rank, local):
             tf = gemm_kernel_timing(isb, lay, xq, mm, "float", iters=10)
             us_i = sum(r["us"] for r in ti)
             us_f = sum(r["us"] for r in tf)
+            us_d = sum(dense_layer_timing(isb, mm, dev, wd, iters=10 if mm <= 256 else 4))
             ops = sum(2 * mm * k * n for _, k, n in LAYER)
             byts = sum(r["alg_bytes"] for r in ti)
             sweep.append({"M": mm, "us_per_layer_int": round(us_i, 2),
                           "us_per_layer_float": round(us_f, 2),
                           "speedup_vs_float": round(us_f / us_i, 3),
+                          "us_per_layer_fp16_dense": round(us_d, 2),
+                          "speedup_vs_fp16_dense": round(us_d / us_i, 3),
                           "tops_int": round(ops / us_i / 1e6, 1),
                           "hbm_frac_int": round(byts / us_i / 1e3 / peak, 3)})
 
@@ -415,6 +454,11 @@ def run_ours(args, ws, rank, local):
                      "layer_frac": round(tot_bytes / tot_us / 1e3 / peak, 4),
                      "per_linear": kt},
         "float_scale_kernel": kf,
+        "fp16_dense": {"kernel": "gemm_f16_tc (tcgen05 kind::f16, fp32 acc, no cuBLAS)",
+                       "us_per_linear": [round(v, 2) for v in dense_m],
+                       "us_per_layer": round(sum(dense_m), 2),
+                       "speedup_w4a8_kernels_vs_fp16": round(sum(dense_m) / tot_us, 3),
+                       "speedup_w4a8_step_vs_fp16": round(sum(dense_m) / (ms_per_step * 1e3), 3)},
         "e2e": {"value": round(ws * ops_per_step / (e2e_ms * 1e-3) / 1e12, 3), "unit": "TOPS",
                 "us_per_layer": round(e2e_ms * 1e3, 2),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -151,6 +151,17 @@ int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t 
                        void* workspace, int64_t workspace_bytes, void* stream);
 
 /* --------------------------------------------------------------------------
+ * Dense fp16 / bf16 baseline GEMM (no reference analogue; BASELINE.json north
+ * star: "an fp16 cuBLAS-free dense baseline kernel ... reported for the paper's
+ * speedup claims"): out[M][N] = x[M][K] * w[N][K]^T (nn.Linear weight layout),
+ * hand-written tcgen05 kind::f16 with fp32 accumulation, TMA-fed, split-K over a
+ * cluster at decode M. x and w share `dtype` (ISB_F16 or ISB_BF16); K % 64 == 0;
+ * 16-byte aligned operands.
+ */
+int isb_gemm_dense(const void* x, const void* w, int dtype, int64_t m, int64_t n, int64_t k,
+                   void* out, int out_dtype, void* stream);
+
+/* --------------------------------------------------------------------------
  * Tensor parallelism (no reference analogue — the reference is one
  * host process). Row-parallel layers shard K on group boundaries: every rank
  * produces the int32 accumulator of its groups (out_dtype = ISB_I32 above),

@@ -440,6 +440,33 @@ int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t 
   });
 }
 
+int isb_gemm_dense(const void* x, const void* w, int dtype, int64_t m, int64_t n, int64_t k,
+                   void* out, int out_dtype, void* stream) {
+  return guarded([&] {
+    if (!x || !w || !out) fail(ISB_PARAM, "null pointer");
+    if (m < 1 || n < 1 || k < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+    if (dtype != ISB_F16 && dtype != ISB_BF16) fail(ISB_PARAM, "dense inputs must be fp16 or bf16");
+    if (out_dtype != ISB_F32 && out_dtype != ISB_BF16 && out_dtype != ISB_F16)
+      fail(ISB_PARAM, "unsupported output dtype");
+    if (k % 64 != 0) fail(ISB_PARAM, "dense GEMM needs K % 64 == 0");
+    if (reinterpret_cast<uintptr_t>(x) % 16 || reinterpret_cast<uintptr_t>(w) % 16)
+      fail(ISB_PARAM, "dense GEMM operands must be 16-byte aligned");
+    if (m > std::numeric_limits<int>::max() || n > std::numeric_limits<int>::max())
+      fail(ISB_PARAM, "shape too large");
+    launch_gemm_dense(x, w, m, n, k, out, out_dtype, dtype == ISB_BF16, num_sms(), as_stream(stream));
+  });
+}
+
+// Measurement only: the dense kernel's pipeline on kind::i8 (int8 x int8 -> float32),
+// x [M][K], w [N][K], K % 128 == 0 — the SS-form upper bound for an int8 K3.
+extern "C" int isb_debug_gemm_dense_i8(const void* x, const void* w, int64_t m, int64_t n,
+                                       int64_t k, float* out, void* stream) {
+  return guarded([&] {
+    if (k % 128 != 0) fail(ISB_PARAM, "K % 128");
+    launch_gemm_dense_i8(x, w, m, n, k, out, num_sms(), as_stream(stream));
+  });
+}
+
 int isb_finalize_acc(const int32_t* acc, const double* sa, int64_t m, int64_t n,
                      int64_t amplifier, void* out, int out_dtype, void* stream) {
   return guarded([&] {

@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(DCfg<MT>::kThreads, DCfg<MT>::kMinBlocks)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             if (i < n) qv[i][c] = ld_shared_v4(w_base + i * kBlockBytes + c * (kTileN * 16));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the async refill
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         mbar_wait(&a_empty[as], ((js / kNA) & 1) ^ 1);
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__(DCfg<MT>::kThreads, DCfg<MT>::kMinBlocks)
           }
         }
         tc_fence_before();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // scale reads before refill
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&d_empty[ds]);

@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) q[c] = ld_shared_v4(w_base + stage * kFStage + c * (kTileN * 16));
       const int32_t k = static_cast<int32_t>(ld_shared_u32(sc_base + stage * kTileN * 4));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the async refill
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       const float kf = static_cast<float>(k);
@@ -326,6 +327,297 @@ __global__ void __launch_bounds__(kFThreads, 1)
   if (warp == 2) tmem_dealloc(tmem_base, 512);
 }
 
+
+// ============================================================================
+// SS variant: the transform warps write the folded int8 weights into a shared-
+// memory ring in the canonical SWIZZLE_128B K-major layout (row = channel,
+// 16-byte chunk c of row r at r*128 + ((c ^ (r & 7)) * 16)) and the MMA reads
+// both operands from shared memory (tcgen05.mma kind::i8, SS form), so TMEM only
+// holds the two int32 accumulators and the tile can be 256 tokens wide.
+template <int MT, int NA = 2, int SX = 4, int SW = 6>
+struct FoldSS {
+  static constexpr int kXBytes = MT * 128;
+  static constexpr int kNA = NA;             // folded-weight ring (16 KiB each)
+  static constexpr int kABytes = 128 * 128;
+  static constexpr int kSX = SX;             // activation ring (consumed by the MMA)
+  static constexpr int kSW = SW;             // packed-weight ring (consumed by the transform)
+  static constexpr int kSmem = 1024 + NA * kABytes + SX * kXBytes + SW * (kBlockBytes + kTileN * 4) +
+                               2 * MT * 8 + 1024;
+  static constexpr int kThreads = 128 + 128 * kFXformWG + 128;
+  static_assert(kXBytes % 1024 == 0, "SW128 tiles need 1 KiB alignment");
+  // Each ring slot must always be served by the same transform warpgroup (slots are
+  // waited on by parity, which only tracks a lead of one phase).
+  static_assert(NA % kFXformWG == 0 && SW % kFXformWG == 0, "ring slots per warpgroup");
+  static_assert(kSmem <= 227 * 1024, "smem");
+  static_assert(2 * MT <= 512, "TMEM");
+};
+
+// Two producer threads keep separate rings: the packed weights (+ k_g) run ahead
+// of the transform warps, the activation tiles are recycled by the MMA alone, so
+// the transform's latency is not part of the activation ring's turnaround.
+template <int MT, int NA, int SX, int SW>
+__global__ void __launch_bounds__(FoldSS<MT, NA, SX, SW>::kThreads, 1)
+    gemm_w4a8_fold_ss(const __grid_constant__ CUtensorMap x_map, const FoldParams p) {
+  using F = FoldSS<MT, NA, SX, SW>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smem_a = smem;                                   // [NA][128 x 128] folded int8
+  uint8_t* smem_x = smem_a + NA * F::kABytes;               // [SX][MT x 128] activations
+  uint8_t* smem_w = smem_x + SX * F::kXBytes;               // [SW][8 KiB] packed weights
+  uint8_t* smem_sc = smem_w + SW * kBlockBytes;             // [SW][128] k_g
+  double* sa_s = reinterpret_cast<double*>(smem_sc + SW * kTileN * 4);  // [2][MT]
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(sa_s + 2 * MT);
+  uint64_t* wempty = wfull + SW;
+  uint64_t* xfull = wempty + SW;
+  uint64_t* xempty = xfull + SX;
+  uint64_t* a_full = xempty + SX;
+  uint64_t* a_empty = a_full + NA;
+  uint64_t* d_full = a_empty + NA;
+  uint64_t* d_empty = d_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int ntiles = static_cast<int>(blockIdx.x) < p.tiles
+                         ? (p.tiles - static_cast<int>(blockIdx.x) + gridDim.x - 1) / gridDim.x
+                         : 0;
+  const int total = ntiles * p.kblocks;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tensormap(&x_map);
+    for (int i = 0; i < SW; ++i) {
+      mbar_init(&wfull[i], 1);
+      mbar_init(&wempty[i], 4);
+    }
+    for (int i = 0; i < SX; ++i) {
+      mbar_init(&xfull[i], 1);
+      mbar_init(&xempty[i], 1);
+    }
+    for (int i = 0; i < NA; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&d_full[i], 1);
+      mbar_init(&d_empty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 2 * MT <= 256 ? 256 : 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) pdl_launch_dependents();
+
+  auto tile_of = [&](int it, int& nt, int& mt) {
+    const int t = blockIdx.x + it * gridDim.x;
+    nt = t / p.m_tiles;
+    mt = t % p.m_tiles;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------ producer: packed weights + k_g
+    if (elect_one()) {
+      for (int j = 0; j < total; ++j) {
+        const int s = j % SW;
+        mbar_wait(&wempty[s], ((j / SW) & 1) ^ 1);
+        int nt, mt;
+        tile_of(j / p.kblocks, nt, mt);
+        const int kb = j % p.kblocks;
+        mbar_arrive_expect_tx(&wfull[s], kBlockBytes + kTileN * 4);
+        bulk_load(smem_w + s * kBlockBytes,
+                  p.packed + (static_cast<int64_t>(nt) * p.kblocks + kb) * kBlockBytes,
+                  kBlockBytes, &wfull[s]);
+        bulk_load(smem_sc + s * kTileN * 4,
+                  p.kscale + (static_cast<int64_t>(nt) * p.G + kb / p.gb) * kTileN, kTileN * 4,
+                  &wfull[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    // ------------------------------------------------ producer: activation tiles
+    if (elect_one()) {
+      pdl_wait();
+      for (int j = 0; j < total; ++j) {
+        const int s = j % SX;
+        mbar_wait(&xempty[s], ((j / SX) & 1) ^ 1);
+        int nt, mt;
+        tile_of(j / p.kblocks, nt, mt);
+        mbar_arrive_expect_tx(&xfull[s], F::kXBytes);
+        tma_load_2d(smem_x + s * F::kXBytes, &x_map, &xfull[s], (j % p.kblocks) * kBlockK, mt * MT);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc = make_idesc_i8(128, MT);
+      int j = 0;
+      for (int it = 0; it < ntiles; ++it) {
+        const int ds = it & 1;
+        mbar_wait(&d_empty[ds], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + ds * MT;
+        for (int kb = 0; kb < p.kblocks; ++kb, ++j) {
+          const int xs = j % SX, as = j % NA;
+          mbar_wait(&a_full[as], (j / NA) & 1);
+          mbar_wait(&xfull[xs], (j / SX) & 1);
+          tc_fence_after();
+          const uint64_t adesc = make_sw128_kmajor_desc(smem_u32(smem_a + as * F::kABytes));
+          const uint64_t bdesc = make_sw128_kmajor_desc(smem_u32(smem_x + xs * F::kXBytes));
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            mma_i8_ss(d_tmem, adesc + static_cast<uint64_t>(c * 2), bdesc + static_cast<uint64_t>(c * 2),
+                      idesc, (kb > 0 || c > 0) ? 1u : 0u);
+          mma_commit(&xempty[xs]);
+          mma_commit(&a_empty[as]);
+        }
+        mma_commit(&d_full[ds]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4 && warp < 4 + 4 * kFXformWG) {
+    // ---------------------------------------------------------------- transform
+    const int xw = static_cast<int>(warp - 4) / 4;
+    const uint32_t r = (warp % 4) * 32 + lane;  // output channel == A row
+    const uint32_t w_base = smem_u32(smem_w) + r * 16;
+    const uint32_t sc_base = smem_u32(smem_sc) + r * 4;
+    const uint32_t a_row = smem_u32(smem_a) + r * 128;
+    for (int j = xw; j < total; j += kFXformWG) {
+      const int s = j % SW, as = j % NA;
+      mbar_wait(&wfull[s], (j / SW) & 1);
+      uint4 q[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) q[c] = ld_shared_v4(w_base + s * kBlockBytes + c * (kTileN * 16));
+      const int32_t k = static_cast<int32_t>(ld_shared_u32(sc_base + s * kTileN * 4));
+      const float kf = static_cast<float>(k);
+      const uint32_t k1 = half2_bits(kf);
+      const uint32_t k16 = half2_bits(kf * 0.0625f);
+      const uint32_t cA = half2_bits(1536.0f - 1032.0f * kf);
+      const uint32_t cB = half2_bits(1536.0f - 72.0f * kf);
+      uint32_t a[32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t w4[4] = {q[c].x, q[c].y, q[c].z, q[c].w};
+#pragma unroll
+        for (int w = 0; w < 4; ++w) fold_word(w4[w], k1, k16, cA, cB, a[c * 8 + 2 * w], a[c * 8 + 2 * w + 1]);
+      }
+      // Release the packed slot only once its values have been consumed: the refill
+      // is an async-proxy bulk copy that must not overtake these shared loads.
+      // generic-proxy reads of the slot ordered before the async-proxy refill
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&wempty[s]);
+      mbar_wait(&a_empty[as], ((j / NA) & 1) ^ 1);
+      const uint32_t dst = a_row + as * F::kABytes;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + ((ch ^ (r & 7)) * 16)),
+                     "r"(a[4 * ch]), "r"(a[4 * ch + 1]), "r"(a[4 * ch + 2]), "r"(a[4 * ch + 3])
+                     : "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
+      named_bar_sync(2 + xw, 128);  // the whole warpgroup's rows are written and fenced
+      if (warp % 4 == 0 && lane == 0) mbar_arrive(&a_full[as]);
+    }
+  } else if (warp >= 4 + 4 * kFXformWG) {
+    // ---------------------------------------------------------------- epilogue
+    const uint32_t ew = warp - (4 + 4 * kFXformWG);
+    const uint32_t t128 = ew * 32 + lane;
+    const uint32_t r = t128;
+    const uint32_t lane_base = (ew * 32) << 16;
+    pdl_wait();
+    auto sa_prefetch = [&](int it) {
+      if (it < ntiles) {
+        int nt, mt;
+        tile_of(it, nt, mt);
+        for (int t = t128; t < MT; t += 128) {
+          const int64_t m = static_cast<int64_t>(mt) * MT + t;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                           smem_u32(sa_s + (it & 1) * MT + t)),
+                       "l"(p.sa + (m < p.M ? m : 0)), "r"(m < p.M ? 8 : 0)
+                       : "memory");
+        }
+      }
+      cp_async_commit();
+    };
+    sa_prefetch(0);
+    for (int it = 0; it < ntiles; ++it) {
+      int nt, mt;
+      tile_of(it, nt, mt);
+      const int ds = it & 1;
+      sa_prefetch(it + 1);
+      cp_async_wait<1>();
+      named_bar_sync(1, 128);
+      const double* sa_t = sa_s + (it & 1) * MT;
+      mbar_wait(&d_full[ds], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + lane_base + ds * MT;
+      const int64_t n = static_cast<int64_t>(nt) * kTileN + r;
+      const int64_t m0 = static_cast<int64_t>(mt) * MT;
+#pragma unroll 1
+      for (int cc = 0; cc < MT; cc += 32) {
+        uint32_t v[32];
+        tmem_ld_x16_(taddr + cc, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+        tmem_ld_x16_(taddr + cc + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+        tmem_wait_ld();
+        if (cc + 32 >= MT) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d_empty[ds]);
+        }
+        if (n < p.N) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int64_t m = m0 + cc + t;
+            if (m < p.M) {
+              if (p.out_dtype == ISB_I32) {
+                static_cast<int32_t*>(p.out)[m * p.N + n] = static_cast<int32_t>(v[t]);
+              } else {
+                const double o = __dmul_rn(
+                    static_cast<double>(static_cast<int32_t>(v[t])) * p.inv_amp, sa_t[cc + t]);
+                store_out_f(p.out, p.out_dtype, m * p.N + n, __double2float_rn(o));
+              }
+            }
+          }
+        }
+      }
+      named_bar_sync(1, 128);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem_base, 2 * MT <= 256 ? 256 : 512);
+}
+
+template <int MT, int NA = 2, int SX = 4, int SW = 6>
+void launch_fold_ss(const int8_t* xq, int64_t m, const isb_weight& w, FoldParams prm, int num_sms,
+                    cudaStream_t s) {
+  using F = FoldSS<MT, NA, SX, SW>;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cuda_check(cudaFuncSetAttribute(gemm_w4a8_fold_ss<MT, NA, SX, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    F::kSmem),
+               "cudaFuncSetAttribute(fold ss smem)");
+  });
+  prm.m_tiles = static_cast<int>((m + MT - 1) / MT);
+  prm.tiles = static_cast<int>(w.n_tiles) * prm.m_tiles;
+  const CUtensorMap map = make_x_map(xq, m, w.k, MT);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min(prm.tiles, num_sms));
+  cfg.blockDim = dim3(F::kThreads);
+  cfg.dynamicSmemBytes = F::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, gemm_w4a8_fold_ss<MT, NA, SX, SW>, map, prm), "gemm_w4a8_fold_ss launch");
+  count_launch();
+}
 
 // ============================================================================
 // 2-SM variant (tcgen05.mma.cta_group::2). A CTA pair computes 256 channels
@@ -542,6 +834,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
         for (int c = 0; c < 4; ++c) q[c] = ld_shared_v4(w_base + stage * k2Stage + c * (kTileN * 16));
         k = static_cast<int32_t>(ld_shared_u32(sc_base + stage * kTileN * 4));
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the async refill
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       uint32_t a[32];
@@ -727,6 +1020,15 @@ void launch_gemm_fold(const int8_t* xq, const double* sa, int64_t m, const isb_w
     launch_fold2(make_x_map(xq, m, w.k, k2MT / 2), p2, num_sms, s);
     return;
   }
+  static const int ss_mt = [] {  // default: SS kernel, 256-token tiles; ISB_FOLD_SS=0: TS kernel
+    const char* e = std::getenv("ISB_FOLD_SS");
+    return e ? std::atoi(e) : 256;
+  }();
+  if (ss_mt == 256) {
+    launch_fold_ss<256, 2, 4, 6>(xq, m, w, prm, num_sms, s);
+    return;
+  }
+
   const CUtensorMap map = make_x_map(xq, m, w.k, kFMT);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(std::min(prm.tiles, num_sms));

@@ -527,6 +527,7 @@ __global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
         for (int c = 0; c < 4; ++c)
           if (i < nkb)
             q[i][c] = ld_shared_v4(w_base + (stage * S + i) * kBlockBytes + c * (kTileN * 16));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the async refill
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       mbar_wait(&a_empty[as], ((j / Cf::kNA) & 1) ^ 1);
@@ -646,6 +647,7 @@ __global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
           }
         }
         tc_fence_before();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // scale reads before refill
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&d_empty[ds]);

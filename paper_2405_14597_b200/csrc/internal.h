@@ -96,6 +96,11 @@ int64_t decode_workspace_bytes(int64_t m, const isb_weight& w);
 void launch_gemm_decode(int path, const int8_t* xq, const double* sa, int64_t m,
                         const isb_weight& w, void* out, int out_dtype, void* workspace,
                         int num_sms, cudaStream_t s);
+// Dense fp16/bf16 baseline (gemm_f16.cu): out = x[M][K] * w[N][K]^T, K % 64 == 0.
+void launch_gemm_dense(const void* x, const void* w, int64_t m, int64_t n, int64_t k, void* out,
+                       int out_dtype, bool bf16, int num_sms, cudaStream_t s);
+void launch_gemm_dense_i8(const void* x, const void* w, int64_t m, int64_t n, int64_t k, void* out,
+                          int num_sms, cudaStream_t s);  // measurement only (SS int8 bound)
 void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                     void* out, int out_dtype, void* workspace, const GemmPlan& plan,
                     cudaStream_t s, const void* xf = nullptr, int x_dtype = 0,

@@ -357,5 +357,24 @@ def gemm_checked(path: str, xq, sa, w: PackedWeight, strict=False, want_f64=True
     return out, of, acc, part, stats
 
 
+def gemm_dense(x: torch.Tensor, w: torch.Tensor, out_dtype=None, out=None, stream=None):
+    """Dense fp16/bf16 baseline (no cuBLAS): x[M][K] @ w[N][K]^T on tcgen05 kind::f16
+    with fp32 accumulation (isb_gemm_dense) — the FP16 comparator of the paper's
+    W4A8 speed-up claims. Same semantics as torch.nn.functional.linear(x, w)."""
+    if x.dtype != w.dtype or x.dtype not in (torch.float16, torch.bfloat16):
+        raise _lib.ParamError("dense operands must both be fp16 or bf16")
+    x = _cuda(x)
+    w = _cuda(w)
+    m, k = x.shape
+    n, k2 = w.shape
+    if k2 != k:
+        raise _lib.DimensionError(f"activation K={k} vs weight K={k2}")
+    if out is None:
+        out = torch.empty((m, n), dtype=out_dtype or x.dtype, device=x.device)
+    check(load().isb_gemm_dense(_ptr(x), _ptr(w), _DT[x.dtype], m, n, k, _ptr(out),
+                                _DT[out.dtype], _stream(stream)))
+    return out
+
+
 def launch_count() -> int:
     return load().isb_launch_count()

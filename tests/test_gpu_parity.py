@@ -190,13 +190,16 @@ def test_workspace_is_left_clean_and_results_repeat():
     assert int(ws.buf.view(torch.int32).abs().sum()) == 0  # split-K workspace left clean
 
 
-def test_fold_2sm_kernel_subprocess():
-    """The opt-in cta_group::2 prefill kernel (ISB_FOLD2=1): bit-exact on the fold tests."""
+@pytest.mark.parametrize("env_kv", [("ISB_FOLD2", "1"), ("ISB_FOLD_SS", "0")],
+                         ids=["cta_group2", "tmem_operand"])
+def test_fold_variant_kernels_subprocess(env_kv):
+    """The opt-in prefill kernels — cta_group::2 pairs (ISB_FOLD2=1) and the TMEM-operand
+    (TS) kernel (ISB_FOLD_SS=0) — bit-exact on the fold tests (read once per process)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, ISB_FOLD2="1")
+    env = dict(os.environ, **{env_kv[0]: env_kv[1]})
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
                         os.path.join(root, "tests", "test_gpu_parity.py"),
                         "-k", "fold and not subprocess"],
