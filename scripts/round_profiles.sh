@@ -11,3 +11,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm
   -o gpurun_out/k3_gu_m16 python scripts/prof_gemm.py 16 4096 22016 int 6 > gpurun_out/ncu_gu.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_w4a8_fold -s 2 -c 1 \
   -o gpurun_out/k3_pf_m2048 python scripts/prof_gemm.py 2048 4096 4096 int 4 > gpurun_out/ncu_pf.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_f16_tc -s 2 -c 1 \
+  -o gpurun_out/dense_pf_m2048 python scripts/dense_timing.py 2048 > gpurun_out/ncu_dense.log 2>&1
