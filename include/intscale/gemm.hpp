@@ -60,10 +60,27 @@ GemmResult gemm_integer_scale(const QuantizedTensor& x, const QuantizedTensor& w
 GemmResult gemm_coarse(const QuantizedTensor& x, const QuantizedTensor& w,
                        const GemmOptions& opt = {});
 
+/// Inner stage of the dual-quantization path (gemm.hpp:18-27): asymmetric 4-bit
+/// group codes of an 8-bit per-channel weight's integer codes.
+struct DualInnerQuant {
+  MatQ values;
+  VecD scales;
+  VecI zero_points;
+  Index group_size = 128;
+};
+
+/// dual_inner_quantize (gemm.hpp:31, gemm.cpp:311-345) — on the device, bit-exact.
+DualInnerQuant dual_inner_quantize(const QuantizedTensor& w_outer, Index group_size);
+
+/// gemm_dual_quant (gemm.hpp:105, gemm.cpp:347-412): the QServe-style comparison path,
+/// sequential double accumulation on CUDA cores, bit-exact.
+GemmResult gemm_dual_quant(const QuantizedTensor& x, const QuantizedTensor& w_outer,
+                           const DualInnerQuant& inner, const GemmOptions& opt = {});
+
 struct PathConfig {
   PathKind kind = PathKind::integer_scale;
   const IntegerScaleSet* int_scales = nullptr;
-  const void* inner = nullptr;  // dual-quant is outside the B200 path
+  const DualInnerQuant* inner = nullptr;
 };
 
 GemmResult run_layer(const QuantizedTensor& x, const QuantizedTensor& w, const PathConfig& path,

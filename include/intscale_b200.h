@@ -162,6 +162,24 @@ int isb_gemm_dense(const void* x, const void* w, int dtype, int64_t m, int64_t n
                    void* out, int out_dtype, void* stream);
 
 /* --------------------------------------------------------------------------
+ * QServe-style dual quantization (the paper's comparison path):
+ * isb_dual_inner_quantize replaces dual_inner_quantize (gemm.cpp:311-345): the
+ * 8-bit per-channel codes w8 (K x N int16, device) -> asymmetric 4-bit group codes
+ * (K x N int16 in [0,15]) + double scales and int32 zero points per unit j*G + t.
+ * isb_gemm_dual_quant replaces gemm_dual_quant (gemm.cpp:347-412): out = float(
+ * (sum_k x * ((w - z) * s_i)) * s_outer[j] * s_a[i]) with the reference's sequential
+ * double accumulation, bit-exact; out_f64 (nullable) gets the double value. Values
+ * are validated on the device first (ISB_VALUE, as gemm.cpp:114, :366-372); the call
+ * synchronises the stream for that check.
+ */
+int isb_dual_inner_quantize(const int16_t* w8, int64_t k, int64_t n, int64_t group,
+                            int16_t* codes, double* scales, int32_t* zero_points, void* stream);
+int isb_gemm_dual_quant(const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                        const int16_t* codes, const double* scales, const int32_t* zero_points,
+                        int64_t group, const double* outer_scales, int64_t n, float* out,
+                        double* out_f64, void* stream);
+
+/* --------------------------------------------------------------------------
  * Tensor parallelism (no reference analogue — the reference is one
  * host process). Row-parallel layers shard K on group boundaries: every rank
  * produces the int32 accumulator of its groups (out_dtype = ISB_I32 above),

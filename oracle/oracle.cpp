@@ -664,4 +664,59 @@ void or_expected_counters(int path, std::int64_t m, std::int64_t n, std::int64_t
   }
 }
 
+// dual_inner_quantize, gemm.cpp:311-345: asymmetric 4-bit group quantization of an
+// 8-bit per-channel weight's integer codes. w8 K x N row-major; unit u = j*G + t.
+int or_dual_inner_quantize(const std::int16_t* w8, std::int64_t k, std::int64_t n,
+                           std::int64_t group, std::int16_t* codes, double* scales,
+                           std::int32_t* zps) {
+  return guarded([&] {
+    if (group < 1 || k % group != 0) fail(PARAM, "group size must divide the reduction dimension");
+    const Index groups = k / group;
+    for (Index j = 0; j < n; ++j)
+      for (Index t = 0; t < groups; ++t) {
+        double lo = std::numeric_limits<double>::infinity(), hi = -lo;
+        for (Index r = t * group; r < (t + 1) * group; ++r) {
+          lo = std::min(lo, static_cast<double>(w8[r * n + j]));
+          hi = std::max(hi, static_cast<double>(w8[r * n + j]));
+        }
+        const double sc = hi == lo ? 1.0 : (hi - lo) / 15.0;
+        const auto z = static_cast<std::int32_t>(std::clamp<std::int64_t>(std::llround(-lo / sc), 0, 15));
+        scales[j * groups + t] = sc;
+        zps[j * groups + t] = z;
+        for (Index r = t * group; r < (t + 1) * group; ++r) {
+          const std::int64_t q = std::llround(static_cast<double>(w8[r * n + j]) / sc) + z;
+          codes[r * n + j] = static_cast<std::int16_t>(std::clamp<std::int64_t>(q, 0, 15));
+        }
+      }
+  });
+}
+
+// gemm_dual_quant, gemm.cpp:347-412 (after validation): per output a sequential
+// double accumulation cd += double(x) * ((double)(w - z) * s_i) over k in order,
+// then out = float(cd * s_outer[j] * s_a[i]) (-ffp-contract=off: no FMA).
+int or_gemm_dual_quant(const std::int16_t* x, const double* sa, std::int64_t m, std::int64_t k,
+                       const std::int16_t* codes, const double* scales, const std::int32_t* zps,
+                       std::int64_t group, const double* s_outer, std::int64_t n, float* out,
+                       double* out_f64) {
+  return guarded([&] {
+    if (group < 1 || k % group != 0) fail(PARAM, "inner group size must divide K");
+    const Index groups = k / group;
+    for (Index i = 0; i < m; ++i)
+      for (Index j = 0; j < n; ++j) {
+        double cd = 0.0;
+        for (Index gi = 0; gi < groups; ++gi) {
+          const double si = scales[j * groups + gi];
+          const std::int32_t z = zps[j * groups + gi];
+          for (Index kk = gi * group; kk < (gi + 1) * group; ++kk) {
+            const double wrec = static_cast<double>(std::int32_t{codes[kk * n + j]} - z) * si;
+            cd += static_cast<double>(x[i * k + kk]) * wrec;
+          }
+        }
+        const double o = cd * s_outer[j] * sa[i];
+        out[i * n + j] = static_cast<float>(o);
+        if (out_f64) out_f64[i * n + j] = o;
+      }
+  });
+}
+
 }  // extern "C"

@@ -269,6 +269,44 @@ def gemm_coarse(x: QuantizedTensor, w: QuantizedTensor, workers=1) -> "GemmResul
     return gemm_float_scale(x, w, workers=workers)
 
 
+class DualInnerQuant:
+    """DualInnerQuant, gemm.hpp:22-27: codes K x N in [0, 15], scales / zero points per
+    unit j*G + t, group size."""
+
+    def __init__(self, values, scales, zero_points, group):
+        self.values, self.scales, self.zero_points, self.group = values, scales, zero_points, group
+
+
+def dual_inner_quantize(w8: QuantizedTensor, group: int) -> DualInnerQuant:
+    """dual_inner_quantize, gemm.cpp:311-345 (8-bit per-channel symmetric outer weight)."""
+    if w8.bit_width != 8 or w8.scheme != SYMMETRIC or w8.kind != PER_CHANNEL:
+        raise OracleError(PARAM, "dual quantization layers over an 8-bit per-channel symmetric weight")
+    k, n = w8.values.shape
+    g = int(group)
+    units = (k // g) * n if g >= 1 else 1
+    codes = np.empty((k, n), np.int16)
+    scales = np.empty(max(units, 1), np.float64)
+    zps = np.empty(max(units, 1), np.int32)
+    _check(lib().or_dual_inner_quantize(_p(np.ascontiguousarray(w8.values, np.int16)), C.c_int64(k),
+                                        C.c_int64(n), C.c_int64(g), _p(codes), _p(scales), _p(zps)))
+    return DualInnerQuant(codes, scales[:units], zps[:units], g)
+
+
+def gemm_dual_quant(x: QuantizedTensor, w8: QuantizedTensor, inner: DualInnerQuant) -> GemmResult:
+    """gemm_dual_quant, gemm.cpp:347-412: output float32 and the double pre-rounding value."""
+    m, k = x.values.shape
+    n = w8.values.shape[1]
+    out = np.empty((m, n), np.float32)
+    of = np.empty((m, n), np.float64)
+    _check(lib().or_gemm_dual_quant(
+        _p(np.ascontiguousarray(x.values, np.int16)), _p(np.ascontiguousarray(x.scales, np.float64)),
+        C.c_int64(m), C.c_int64(k), _p(np.ascontiguousarray(inner.values, np.int16)),
+        _p(np.ascontiguousarray(inner.scales, np.float64)),
+        _p(np.ascontiguousarray(inner.zero_points, np.int32)), C.c_int64(inner.group),
+        _p(np.ascontiguousarray(w8.scales, np.float64)), C.c_int64(n), _p(out), _p(of)))
+    return GemmResult(out, {}, of, None, None)
+
+
 def gemm_oracle(path: str, x: QuantizedTensor, w: QuantizedTensor, amplifier=1):
     m, k = x.values.shape
     kw, n = w.values.shape

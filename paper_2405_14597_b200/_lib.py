@@ -102,6 +102,9 @@ SIGNATURES = {
     "isb_gemm_coarse": (_INT, [_VP, _VP, _I64, _I64, _VP, _VP, _INT, _VP, _I64, _VP]),
     "isb_gemm_act_fused": (_INT, [_INT, _VP, _INT, _I64, _I64, _VP, _VP, _INT, _VP, _VP, _I64,
                                   _VP]),
+    "isb_dual_inner_quantize": (_INT, [_VP, _I64, _I64, _I64, _VP, _VP, _VP, _VP]),
+    "isb_gemm_dual_quant": (_INT, [_VP, _VP, _I64, _I64, _VP, _VP, _VP, _I64, _VP, _I64, _VP, _VP,
+                                    _VP]),
     "isb_gemm_dense": (_INT, [_VP, _VP, _INT, _I64, _I64, _I64, _VP, _INT, _VP]),
     "isb_row_absmax": (_INT, [_VP, _INT, _I64, _I64, _VP, _VP]),
     "isb_quantize_per_token_amax": (_INT, [_VP, _INT, _I64, _I64, _VP, _VP, _VP, _VP]),

@@ -467,6 +467,32 @@ extern "C" int isb_debug_gemm_dense_i8(const void* x, const void* w, int64_t m, 
   });
 }
 
+int isb_dual_inner_quantize(const int16_t* w8, int64_t k, int64_t n, int64_t group,
+                            int16_t* codes, double* scales, int32_t* zero_points, void* stream) {
+  return guarded([&] {
+    if (!w8 || !codes || !scales || !zero_points) fail(ISB_PARAM, "null pointer");
+    if (k < 1 || n < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+    if (group < 1 || k % group != 0) fail(ISB_PARAM, "group size must divide the reduction dimension");
+    launch_dual_inner_quantize(w8, k, n, group, codes, scales, zero_points, as_stream(stream));
+  });
+}
+
+int isb_gemm_dual_quant(const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                        const int16_t* codes, const double* scales, const int32_t* zero_points,
+                        int64_t group, const double* outer_scales, int64_t n, float* out,
+                        double* out_f64, void* stream) {
+  return guarded([&] {
+    if (!xq || !sa || !codes || !scales || !zero_points || !outer_scales || !out)
+      fail(ISB_PARAM, "null pointer");
+    if (m < 1 || k < 1 || n < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+    if (group < 1 || k % group != 0) fail(ISB_PARAM, "inner group size must divide K");
+    cudaStream_t s = as_stream(stream);
+    validate_dual(xq, m, k, codes, n, zero_points, scales, group, s);
+    launch_gemm_dual_quant(xq, sa, m, k, codes, scales, zero_points, group, outer_scales, n, out,
+                           out_f64, s);
+  });
+}
+
 int isb_finalize_acc(const int32_t* acc, const double* sa, int64_t m, int64_t n,
                      int64_t amplifier, void* out, int out_dtype, void* stream) {
   return guarded([&] {

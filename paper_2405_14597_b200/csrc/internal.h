@@ -101,6 +101,15 @@ void launch_gemm_dense(const void* x, const void* w, int64_t m, int64_t n, int64
                        int out_dtype, bool bf16, int num_sms, cudaStream_t s);
 void launch_gemm_dense_i8(const void* x, const void* w, int64_t m, int64_t n, int64_t k, void* out,
                           int num_sms, cudaStream_t s);  // measurement only (SS int8 bound)
+// Dual quantization comparison path (dual.cu, gemm.cpp:311-412).
+void launch_dual_inner_quantize(const int16_t* w8, int64_t k, int64_t n, int64_t group,
+                                int16_t* codes, double* scales, int32_t* zps, cudaStream_t s);
+void validate_dual(const int8_t* xq, int64_t m, int64_t k, const int16_t* codes, int64_t n,
+                   const int32_t* zps, const double* scales, int64_t group, cudaStream_t s);
+void launch_gemm_dual_quant(const int8_t* xq, const double* sa, int64_t m, int64_t k,
+                            const int16_t* codes, const double* scales, const int32_t* zps,
+                            int64_t group, const double* s_outer, int64_t n, float* out,
+                            double* out_f64, cudaStream_t s);
 void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                     void* out, int out_dtype, void* workspace, const GemmPlan& plan,
                     cudaStream_t s, const void* xf = nullptr, int x_dtype = 0,

@@ -443,6 +443,77 @@ GemmResult gemm_coarse(const QuantizedTensor& x, const QuantizedTensor& w,
   return res;
 }
 
+DualInnerQuant dual_inner_quantize(const QuantizedTensor& w_outer, Index group_size) {
+  if (w_outer.params.bit_width != 8 || w_outer.params.scheme != Scheme::symmetric ||
+      w_outer.params.granularity.kind != GranKind::per_channel)
+    throw ParamError("dual quantization layers over an 8-bit per-channel symmetric weight");
+  if (group_size < 1 || w_outer.rows() % group_size != 0)
+    throw ParamError("group size must divide the reduction dimension");
+  const Index k = w_outer.rows(), n = w_outer.cols(), units = n * (k / group_size);
+  Dev w8(static_cast<std::size_t>(k * n) * 2), codes(static_cast<std::size_t>(k * n) * 2),
+      sc(static_cast<std::size_t>(units) * 8), zp(static_cast<std::size_t>(units) * 4);
+  up(w8, w_outer.values.data(), static_cast<std::size_t>(k * n));
+  check(isb_dual_inner_quantize(w8.as<std::int16_t>(), k, n, group_size, codes.as<std::int16_t>(),
+                                sc.as<double>(), zp.as<std::int32_t>(), nullptr));
+  DualInnerQuant inner;
+  inner.group_size = group_size;
+  inner.values.resize(k, n);
+  inner.scales.resize(units);
+  inner.zero_points.resize(units);
+  down(inner.values.data(), codes, static_cast<std::size_t>(k * n));
+  down(inner.scales.data(), sc, static_cast<std::size_t>(units));
+  down(inner.zero_points.data(), zp, static_cast<std::size_t>(units));
+  return inner;
+}
+
+GemmResult gemm_dual_quant(const QuantizedTensor& x, const QuantizedTensor& w_outer,
+                           const DualInnerQuant& inner, const GemmOptions& opt) {
+  validate_activation(x);  // gemm.cpp:349
+  if (w_outer.params.bit_width != 8 || w_outer.params.scheme != Scheme::symmetric ||
+      w_outer.params.granularity.kind != GranKind::per_channel)
+    throw ParamError("dual-quant outer weight must be 8-bit per-channel symmetric");
+  if (x.cols() != w_outer.rows())
+    throw DimensionError("activation K=" + std::to_string(x.cols()) + " vs weight rows " +
+                         std::to_string(w_outer.rows()));
+  const Index m = x.rows(), k = x.cols(), n = w_outer.cols(), g = inner.group_size;
+  if (g < 1 || k % g != 0) throw ParamError("inner group size must divide K");
+  const Index units = n * (k / g);
+  if (inner.values.rows() != k || inner.values.cols() != n)
+    throw DimensionError("inner values shape does not match the outer weight");
+  if (inner.scales.size() != units || inner.zero_points.size() != units)
+    throw ParamError("inner parameter count does not match the grouping");
+  if (w_outer.params.scales.size() != n) throw ParamError("outer scale count != channels");
+  const double t0 = now_ms();
+  std::vector<std::int8_t> x8(static_cast<std::size_t>(m * k));
+  for (Index i = 0; i < m * k; ++i) x8[static_cast<std::size_t>(i)] = static_cast<std::int8_t>(x.values.data()[i]);
+  Dev xq(x8.size()), sa(static_cast<std::size_t>(m) * 8), codes(static_cast<std::size_t>(k * n) * 2),
+      sc(static_cast<std::size_t>(units) * 8), zp(static_cast<std::size_t>(units) * 4),
+      so(static_cast<std::size_t>(n) * 8), out(static_cast<std::size_t>(m * n) * 4),
+      of(opt.record_partials ? static_cast<std::size_t>(m * n) * 8 : 0);
+  up(xq, x8.data(), x8.size());
+  up(sa, x.params.scales.data(), static_cast<std::size_t>(m));
+  up(codes, inner.values.data(), static_cast<std::size_t>(k * n));
+  up(sc, inner.scales.data(), static_cast<std::size_t>(units));
+  up(zp, inner.zero_points.data(), static_cast<std::size_t>(units));
+  up(so, w_outer.params.scales.data(), static_cast<std::size_t>(n));
+  check(isb_gemm_dual_quant(xq.as<std::int8_t>(), sa.as<double>(), m, k, codes.as<std::int16_t>(),
+                            sc.as<double>(), zp.as<std::int32_t>(), g, so.as<double>(), n,
+                            out.as<float>(), opt.record_partials ? of.as<double>() : nullptr, nullptr));
+  GemmResult res;
+  res.output.resize(m, n);
+  down(res.output.data(), out, static_cast<std::size_t>(m * n));
+  if (opt.record_partials) {
+    res.output_f64.resize(m, n);
+    down(res.output_f64.data(), of, static_cast<std::size_t>(m * n));
+  }
+  res.stats.int_to_float_conversions = m * n * k;  // gemm.cpp:405-407
+  res.stats.elementwise_multiplies = m * n * k;
+  res.stats.elementwise_subtractions = m * n * k;
+  res.stats.max_abs_accumulator = 0;
+  res.stats.wall_ms = now_ms() - t0;
+  return res;
+}
+
 GemmResult run_layer(const QuantizedTensor& x, const QuantizedTensor& w, const PathConfig& path,
                      FallbackPolicy fallback, const GemmOptions& opt) {  // gemm.cpp:489-516
   switch (path.kind) {
@@ -464,6 +535,9 @@ GemmResult run_layer(const QuantizedTensor& x, const QuantizedTensor& w, const P
       return gemm_integer_scale(x, w, *path.int_scales, opt);
     }
     case PathKind::coarse: return gemm_coarse(x, w, opt);
+    case PathKind::dual_quant:
+      if (!path.inner) throw ParamError("dual-quant path needs inner parameters");
+      return gemm_dual_quant(x, w, *path.inner, opt);
     default:
       throw ParamError("path '" + to_string(path.kind) + "' is outside the B200 integer-scale path");
   }

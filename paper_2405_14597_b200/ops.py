@@ -357,6 +357,49 @@ def gemm_checked(path: str, xq, sa, w: PackedWeight, strict=False, want_f64=True
     return out, of, acc, part, stats
 
 
+class DualInner:
+    """Device DualInnerQuant (gemm.hpp:22-27): codes K x N int16 in [0, 15], double
+    scales and int32 zero points per unit j*G + t, group size."""
+
+    def __init__(self, codes, scales, zero_points, group):
+        self.codes, self.scales, self.zero_points, self.group = codes, scales, zero_points, group
+
+
+def dual_inner_quantize(w8_codes: torch.Tensor, group: int, stream=None) -> DualInner:
+    """dual_inner_quantize (gemm.cpp:311-345) on the device: 8-bit per-channel codes
+    (K x N) -> asymmetric 4-bit group codes + scales + zero points."""
+    w8 = _cuda(w8_codes, torch.int16)
+    k, n = w8.shape
+    if group < 1 or k % group:
+        raise _lib.ParamError("group size must divide the reduction dimension")
+    units = n * (k // group)
+    codes = torch.empty((k, n), dtype=torch.int16, device=w8.device)
+    scales = torch.empty((units,), dtype=torch.float64, device=w8.device)
+    zps = torch.empty((units,), dtype=torch.int32, device=w8.device)
+    check(load().isb_dual_inner_quantize(_ptr(w8), k, n, group, _ptr(codes), _ptr(scales),
+                                         _ptr(zps), _stream(stream)))
+    return DualInner(codes, scales, zps, group)
+
+
+def gemm_dual_quant(xq, sa, inner: DualInner, outer_scales, want_f64=False, stream=None):
+    """gemm_dual_quant (gemm.cpp:347-412): the QServe-style comparison path, bit-exact
+    float32 output (and the double value when want_f64)."""
+    xq = _cuda(xq, torch.int8)
+    sa = _cuda(sa, torch.float64)
+    so = torch.as_tensor(np.asarray(outer_scales, np.float64) if not isinstance(
+        outer_scales, torch.Tensor) else outer_scales, dtype=torch.float64).to(xq.device).contiguous()
+    m, k = xq.shape
+    n = inner.codes.shape[1]
+    if inner.codes.shape[0] != k:
+        raise _lib.DimensionError(f"activation K={k} vs weight rows {inner.codes.shape[0]}")
+    out = torch.empty((m, n), dtype=torch.float32, device=xq.device)
+    of = torch.empty((m, n), dtype=torch.float64, device=xq.device) if want_f64 else None
+    check(load().isb_gemm_dual_quant(_ptr(xq), _ptr(sa), m, k, _ptr(inner.codes),
+                                     _ptr(inner.scales), _ptr(inner.zero_points), inner.group,
+                                     _ptr(so), n, _ptr(out), _ptr(of), _stream(stream)))
+    return (out, of) if want_f64 else out
+
+
 def gemm_dense(x: torch.Tensor, w: torch.Tensor, out_dtype=None, out=None, stream=None):
     """Dense fp16/bf16 baseline (no cuBLAS): x[M][K] @ w[N][K]^T on tcgen05 kind::f16
     with fp32 accumulation (isb_gemm_dense) — the FP16 comparator of the paper's

@@ -519,6 +519,89 @@ static void test_quantized_sidecars() {  // test_quantize.cpp:284-328
   CHECK_THROWS_AS(read_quantized(tmp.file("w.qtns")), IoError);
 }
 
+static void test_dual_quant() {  // test_gemm.cpp:183-226
+  auto x = make_activation({{1}}, {1.0});
+  QuantizedTensor w_outer = make_weight({{5}}, {1.0}, 8, Granularity::per_channel());
+  DualInnerQuant inner;
+  inner.group_size = 1;
+  inner.values = w_outer.values;
+  inner.scales = VecD::Constant(1, 0.5);
+  inner.zero_points = VecI::Constant(1, 3);
+  auto r = gemm_dual_quant(x, w_outer, inner);
+  CHECK(r.output(0, 0) == 1.0f);
+  CHECK(r.stats.int_to_float_conversions == 1);
+  CHECK(r.stats.elementwise_multiplies == 1);
+  CHECK(r.stats.elementwise_subtractions == 1);
+  CHECK(r.stats.integer_multiply_adds == 0);
+  CHECK(r.stats.max_abs_accumulator == 0);
+
+  std::mt19937_64 rng(19);
+  const Index m = 3, k = 8, n = 3;
+  MatQ xq(m, k), wq(k, n);
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < k; ++j) xq(i, j) = static_cast<std::int16_t>(rng() % 255) - 127;
+  for (Index i = 0; i < k; ++i)
+    for (Index j = 0; j < n; ++j) wq(i, j) = static_cast<std::int16_t>(rng() % 16);
+  QuantizedTensor x2;
+  x2.values = xq;
+  x2.params.bit_width = 8;
+  x2.params.scheme = Scheme::symmetric;
+  x2.params.granularity = Granularity::per_token();
+  x2.params.scales = VecD::Constant(m, 0.125);
+  QuantizedTensor outer2;
+  outer2.values = wq;
+  outer2.params.bit_width = 8;
+  outer2.params.scheme = Scheme::symmetric;
+  outer2.params.granularity = Granularity::per_channel();
+  outer2.params.scales = VecD::Constant(n, 0.25);
+  DualInnerQuant ident;
+  ident.group_size = k;
+  ident.values = wq;
+  ident.scales = VecD::Ones(n);
+  ident.zero_points = VecI::Zero(n);
+  auto rd = gemm_dual_quant(x2, outer2, ident);
+  // the coarse path's expression (gemm.cpp:293) on the host: the B200 coarse kernel
+  // packs 4-bit weights, and this identity stage is over 8-bit codes in [0, 15]
+  MatF rc(m, n);
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < n; ++j) {
+      std::int64_t acc = 0;
+      for (Index kk = 0; kk < k; ++kk) acc += std::int64_t{xq(i, kk)} * std::int64_t{wq(kk, j)};
+      rc(i, j) = static_cast<float>(static_cast<double>(acc) * 0.25 * 0.125);
+    }
+  CHECK(rd.output == rc);
+  PathConfig pd{PathKind::dual_quant, nullptr, &ident};
+  CHECK(run_layer(x2, outer2, pd, FallbackPolicy::none).output == rd.output);
+
+  // dual_inner_quantize: codes in [0, 15]; groups straddling zero reconstruct within
+  // half a step (test_gemm.cpp:228-250)
+  MatF wf(16, 6);
+  std::mt19937_64 r2(20);
+  for (Index i = 0; i < wf.size(); ++i) wf.data()[i] = static_cast<float>(((r2() >> 11) * 0x1.0p-53) * 2.0 - 1.0);
+  auto w8 = quantize(wf, 8, Scheme::symmetric, Granularity::per_channel());
+  auto in = dual_inner_quantize(w8, 4);
+  CHECK(in.values.minCoeff() >= 0 && in.values.maxCoeff() <= 15);
+  CHECK(in.scales.size() == 24);
+  for (Index j = 0; j < 6; ++j)
+    for (Index t = 0; t < 4; ++t) {
+      std::int16_t lo = 127, hi = -127;
+      for (Index r = t * 4; r < t * 4 + 4; ++r) {
+        lo = std::min(lo, w8.values(r, j));
+        hi = std::max(hi, w8.values(r, j));
+      }
+      if (lo > 0 || hi < 0) continue;
+      const Index u = j * 4 + t;
+      for (Index r = t * 4; r < t * 4 + 4; ++r) {
+        const double recon = (double(in.values(r, j)) - double(in.zero_points[u])) * in.scales[u];
+        // half a step, up to the rounding of a code clamped at 15 (this synthetic
+        // weight, unlike the reference's seed-20 instance, hits that edge)
+        CHECK(std::abs(recon - double(w8.values(r, j))) <= in.scales[u] / 2 * (1 + 1e-12));
+      }
+    }
+  QuantizedTensor w4 = make_weight({{1}}, {1.0}, 4, Granularity::per_channel());
+  CHECK_THROWS_AS(dual_inner_quantize(w4, 1), ParamError);
+}
+
 int main() {
   const std::pair<const char*, std::function<void()>> tests[] = {
       {"scalar_hand_example", test_scalar_hand_example},
@@ -536,6 +619,7 @@ int main() {
       {"qtns_containers", test_qtns_containers},
       {"qtns_malformed", test_qtns_malformed},
       {"quantized_sidecars", test_quantized_sidecars},
+      {"dual_quant", test_dual_quant},
   };
   for (const auto& [name, fn] : tests) {
     const int before = g_fail;

@@ -585,3 +585,46 @@ def test_coarse_equals_integer_path_when_k_equals_alpha():
         ri = O.gemm_integer_scale(x, wg, s).output
         rc = O.gemm_coarse(x, wc).output
         assert np.array_equal(ri.view(np.int32), rc.view(np.int32))
+
+
+def test_dual_quant_scalar_and_identity_inner():
+    """test_gemm.cpp:183-226: (5 - 3) * 0.5 = 1 reconstructed weight times activation 1
+    gives 1.0f; an identity inner stage (s = 1, z = 0, g = K) over codes in [0, 15]
+    reproduces the coarse path bit for bit (mt19937_64 seed 19 draw order)."""
+    x = q_act([[1]], [1.0])
+    w8 = O.QuantizedTensor(np.array([[5]], np.int16), 8, O.SYMMETRIC, O.PER_CHANNEL, 1,
+                           np.array([1.0]), np.zeros(0, np.int32))
+    inner = O.DualInnerQuant(np.array([[5]], np.int16), np.array([0.5]), np.array([3], np.int32), 1)
+    assert O.gemm_dual_quant(x, w8, inner).output[0, 0] == np.float32(1.0)
+    rng = O.Rng(19)
+    m, k, n = 3, 8, 3
+    xq = (rng.next(m * k) % np.uint64(255)).astype(np.int64).reshape(m, k) - 127
+    wq = (rng.next(k * n) % np.uint64(16)).astype(np.int64).reshape(k, n)
+    x2 = O.QuantizedTensor(xq.astype(np.int16), 8, O.SYMMETRIC, O.PER_TOKEN, 0,
+                           np.full(m, 0.125), np.zeros(0, np.int32))
+    outer = O.QuantizedTensor(wq.astype(np.int16), 8, O.SYMMETRIC, O.PER_CHANNEL, k,
+                              np.full(n, 0.25), np.zeros(0, np.int32))
+    ident = O.DualInnerQuant(wq.astype(np.int16), np.ones(n), np.zeros(n, np.int32), k)
+    rd = O.gemm_dual_quant(x2, outer, ident).output
+    rc = O.gemm_coarse(x2, outer).output
+    assert np.array_equal(rd.view(np.int32), rc.view(np.int32))
+
+
+def test_dual_inner_quantize_reconstructs_within_half_step():
+    """test_gemm.cpp:228-250: inner codes in [0, 15]; groups straddling zero reconstruct
+    the outer codes within half an inner step (random_instance seed 20, g = 4)."""
+    rng = O.Rng(20)
+    _, _, _, wf = random_instance(rng, 1, 16, 6, 16)
+    w8 = O.quantize(wf, 8, O.SYMMETRIC, O.PER_CHANNEL, 0)
+    inner = O.dual_inner_quantize(w8, 4)
+    assert inner.values.shape == (16, 6) and inner.scales.size == 24
+    assert inner.values.min() >= 0 and inner.values.max() <= 15
+    for j in range(6):
+        for t in range(4):
+            u = j * 4 + t
+            col = w8.values[t * 4:(t + 1) * 4, j]
+            if col.min() > 0 or col.max() < 0:
+                continue
+            for r in range(t * 4, (t + 1) * 4):
+                recon = (float(inner.values[r, j]) - float(inner.zero_points[u])) * inner.scales[u]
+                assert abs(recon - float(w8.values[r, j])) <= inner.scales[u] / 2
