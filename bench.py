@@ -411,7 +411,11 @@ def run_ours(args, ws, rank, local):
                           "us_per_layer_fp16_dense": round(us_d, 2),
                           "speedup_vs_fp16_dense": round(us_d / us_i, 3),
                           "tops_int": round(ops / us_i / 1e6, 1),
-                          "hbm_frac_int": round(byts / us_i / 1e3 / peak, 3)})
+                          "hbm_frac_int": round(byts / us_i / 1e3 / peak, 3),
+                          # int8 tensor roofline: nominal 4.5 POPS; measured 4.79 POPS
+                          # (tcgen05 kind::i8 128x256, profiles/r01_mma_peak.txt)
+                          "tensor_frac_int_nominal": round(ops / us_i / 1e6 / 4500.0, 3),
+                          "tensor_frac_int_measured": round(ops / us_i / 1e6 / 4786.0, 3)})
 
     # ---- Mixtral-8x7B expert FFN (config C5): 8 experts on this GPU, T=16 decode
     # tokens top-2 routed (32 expert rows, 4 per expert), per expert K1 + gate/up

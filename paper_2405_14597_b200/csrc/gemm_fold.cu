@@ -565,7 +565,11 @@ __global__ void __launch_bounds__(FoldSS<MT, NA, SX, SW, EW>::kThreads, 1)
 #pragma unroll
           for (int t = 0; t < 32; ++t) {
             const double o = static_cast<double>(static_cast<int32_t>(v[t])) * sa_t[cc + t];
-            po[static_cast<int64_t>(t) * p.N] = __float2bfloat16_rn(__double2float_rn(o));
+            // streaming store: the output is written once and must not evict the
+            // activation tiles every N-tile CTA re-reads from L2
+            const uint16_t b = __bfloat16_as_ushort(__float2bfloat16_rn(__double2float_rn(o)));
+            asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(po + static_cast<int64_t>(t) * p.N), "h"(b)
+                         : "memory");
           }
         } else {
 #pragma unroll
