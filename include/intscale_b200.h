@@ -122,8 +122,11 @@ int isb_weight_info(const isb_weight* w, isb_weight_info_t* info);
  * xq: int8 codes M x K; sa: double[M]. out: M x N in out_dtype.
  * Requires K % 128 == 0 and group % 128 == 0 (isb_weight_info.tensor_core_ok);
  * other shapes => ISB_PARAM (use isb_gemm_checked).
- * The integer path does NOT check overflow: callers gate it with
- * overflow_analyzer (analysis.cpp:24-59) as run_layer does (gemm.cpp:489-516).
+ * Overflow gate: the integer path accumulates in int32, which is exact iff the
+ * weight's overflow_analyzer bound (analysis.cpp:24-59, computed at pack time)
+ * fits int32; an unsafe weight returns ISB_OVERFLOW instead of wrapping (the
+ * exact int64 path is isb_gemm_checked; run_layer falls back to float scale,
+ * gemm.cpp:489-516).
  * workspace: caller-owned device buffer of isb_gemm_workspace_size() bytes,
  * zero-filled once before first use (the kernels leave it zeroed).
  */
@@ -149,6 +152,9 @@ int isb_gemm_float_scale(const int8_t* xq, const double* sa, int64_t m, int64_t 
 int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t k,
                        const isb_weight* w, void* out, int out_dtype, double* sa_out,
                        void* workspace, int64_t workspace_bytes, void* stream);
+/* Workspace for isb_gemm_act_fused: the GEMM's plus room for the int8 codes and
+ * double scales of the two-kernel form (never allocated inside the call). */
+int isb_gemm_act_fused_workspace_size(int64_t m, const isb_weight* w, int64_t* bytes);
 
 /* --------------------------------------------------------------------------
  * Dense fp16 / bf16 baseline GEMM (no reference analogue; BASELINE.json north

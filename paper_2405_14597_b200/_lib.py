@@ -90,6 +90,7 @@ SIGNATURES = {
     "isb_weight_destroy": (_INT, [_VP]),
     "isb_weight_info": (_INT, [_VP, C.POINTER(WeightInfo)]),
     "isb_gemm_workspace_size": (_INT, [_I64, _VP, C.POINTER(_I64)]),
+    "isb_gemm_act_fused_workspace_size": (_INT, [_I64, _VP, C.POINTER(_I64)]),
     "isb_gemm_integer_scale": (_INT, [_VP, _VP, _I64, _I64, _VP, _VP, _INT, _VP, _I64, _VP]),
     "isb_gemm_float_scale": (_INT, [_VP, _VP, _I64, _I64, _VP, _VP, _INT, _VP, _I64, _VP]),
     "isb_gemm_checked": (_INT, [_INT, _VP, _VP, _I64, _I64, _VP, _INT, _VP, _VP, _VP, _VP,

@@ -187,6 +187,20 @@ bool decode_disabled() {
   return off;
 }
 
+int64_t align256(int64_t b) { return (b + 255) / 256 * 256; }
+
+int64_t gemm_workspace_bytes(int64_t m, const isb_weight& w) {
+  if (!w.tensor_core_ok()) return 0;
+  if (decode_eligible(m, w) && !decode_disabled()) return decode_workspace_bytes(m, w);
+  return std::max(plan_gemm(m, w, num_sms(), ISB_PATH_INTEGER_SCALE).workspace_bytes,
+                  plan_gemm(m, w, num_sms(), ISB_PATH_FLOAT_SCALE).workspace_bytes);
+}
+
+// act-fused two-kernel form: GEMM workspace, then s_a [m] doubles, then codes [m][k].
+int64_t act_fused_workspace_bytes(int64_t m, const isb_weight& w) {
+  return align256(gemm_workspace_bytes(m, w)) + align256(8 * m) + align256(m * w.k);
+}
+
 void require_gemm_args(const int8_t* xq, const double* sa, int64_t m, int64_t k,
                        const isb_weight* w, int out_dtype) {
   if (!w) fail(ISB_PARAM, "null weight handle");
@@ -200,6 +214,19 @@ void require_gemm_args(const int8_t* xq, const double* sa, int64_t m, int64_t k,
     fail(ISB_PARAM, "unsupported output dtype");
 }
 
+// The tensor-core integer path accumulates sum_g P_g k_g in int32 (TMEM, registers,
+// the int32 split-K exchange). That equals the reference's int64 acc only while
+// overflow_analyzer's static bound fits int32 (analysis.cpp:24-59); otherwise the
+// device sum could wrap where the reference flags / throws (gemm.cpp:42-52, :90-98).
+// Unsafe layers are refused with ISB_OVERFLOW: the exact int64 path is
+// isb_gemm_checked, and run_layer's float-scale fallback (gemm.cpp:489-516).
+void require_int32_safe(const isb_weight* w) {
+  if (w->static_bound > std::numeric_limits<int32_t>::max())
+    fail(ISB_OVERFLOW, "static overflow bound " + std::to_string(w->static_bound) +
+                           " exceeds int32: the tensor-core integer-scale GEMM cannot be exact "
+                           "for this layer (use isb_gemm_checked or the float-scale fallback)");
+}
+
 void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
              const isb_weight* w, void* out, int out_dtype, void* ws, int64_t ws_bytes,
              void* stream) {
@@ -210,6 +237,7 @@ void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
     fail(ISB_PARAM, "integer-scale path needs an IntegerScaleSet");
   if (out_dtype == ISB_I32 && path != ISB_PATH_INTEGER_SCALE)
     fail(ISB_PARAM, "raw int32 accumulator output exists only on the integer-scale path");
+  if (path == ISB_PATH_INTEGER_SCALE) require_int32_safe(w);
   if (m > std::numeric_limits<int>::max() || w->n > std::numeric_limits<int>::max())
     fail(ISB_PARAM, "shape too large");
   if (decode_eligible(m, *w) && !decode_disabled()) {
@@ -353,11 +381,7 @@ int isb_gemm_workspace_size(int64_t m, const isb_weight* w, int64_t* bytes) {
   return guarded([&] {
     if (!w || !bytes) fail(ISB_PARAM, "null pointer");
     if (m < 1) fail(ISB_PARAM, "shape must be at least 1x1");
-    *bytes = !w->tensor_core_ok() ? 0
-             : decode_eligible(m, *w) && !decode_disabled()
-                 ? decode_workspace_bytes(m, *w)
-                 : std::max(plan_gemm(m, *w, num_sms(), ISB_PATH_INTEGER_SCALE).workspace_bytes,
-                            plan_gemm(m, *w, num_sms(), ISB_PATH_FLOAT_SCALE).workspace_bytes);
+    *bytes = gemm_workspace_bytes(m, *w);
   });
 }
 
@@ -414,6 +438,7 @@ int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t 
       fail(ISB_PARAM, "unknown path");
     if (path == ISB_PATH_INTEGER_SCALE && !w->has_int_scales)
       fail(ISB_PARAM, "integer-scale path needs an IntegerScaleSet");
+    if (path == ISB_PATH_INTEGER_SCALE) require_int32_safe(w);
     if (out_dtype != ISB_F32 && out_dtype != ISB_BF16 && out_dtype != ISB_F16)
       fail(ISB_PARAM, "unsupported output dtype");
     cudaStream_t s = as_stream(stream);
@@ -424,19 +449,28 @@ int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t 
                      sa_out);
       return;
     }
-    // Unfused: K1 into stream-ordered temporaries, then the GEMM.
-    int8_t* codes = nullptr;
-    double* sa = nullptr;
-    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&codes), m * k, s), "cudaMallocAsync");
-    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&sa), m * sizeof(double), s),
-               "cudaMallocAsync");
+    // Unfused: K1 into the caller's workspace (after the GEMM's part), then the GEMM.
+    const int64_t gemm_ws = gemm_workspace_bytes(m, *w);
+    if (!workspace || workspace_bytes < act_fused_workspace_bytes(m, *w))
+      fail(ISB_PARAM, "workspace too small: need " +
+                          std::to_string(act_fused_workspace_bytes(m, *w)) +
+                          " bytes (isb_gemm_act_fused_workspace_size)");
+    auto* base = static_cast<uint8_t*>(workspace);
+    double* sa = reinterpret_cast<double*>(base + align256(gemm_ws));
+    int8_t* codes = reinterpret_cast<int8_t*>(base + align256(gemm_ws) + align256(8 * m));
     launch_quantize_per_token(x, x_dtype, m, k, codes, sa, scratch_flag(), s);
     if (sa_out)
       cuda_check(cudaMemcpyAsync(sa_out, sa, m * sizeof(double), cudaMemcpyDeviceToDevice, s),
                  "copy scales");
-    gemm_tc(path, codes, sa, m, k, w, out, out_dtype, workspace, workspace_bytes, stream);
-    cudaFreeAsync(codes, s);
-    cudaFreeAsync(sa, s);
+    gemm_tc(path, codes, sa, m, k, w, out, out_dtype, workspace, gemm_ws, stream);
+  });
+}
+
+int isb_gemm_act_fused_workspace_size(int64_t m, const isb_weight* w, int64_t* bytes) {
+  return guarded([&] {
+    if (!w || !bytes) fail(ISB_PARAM, "null pointer");
+    if (m < 1) fail(ISB_PARAM, "shape must be at least 1x1");
+    *bytes = act_fused_workspace_bytes(m, *w);
   });
 }
 

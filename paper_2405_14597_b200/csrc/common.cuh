@@ -344,12 +344,19 @@ ISB_DEVICE uint32_t mapa_shared(uint32_t local_addr, uint32_t rank) {
   return r;
 }
 
-// Relaxed remote arrive: callers only publish shared-memory data that was already
-// performed before a CTA-scope release/acquire (so it is in the owning SM's smem
-// when the peer reads it over DSMEM), or retire DSMEM loads whose values were
-// consumed. Avoids the GPU-scope MEMBAR a .release.cluster arrive costs.
+// Relaxed remote arrive: only for retiring DSMEM loads whose values were already
+// consumed ("done reading your buffer"); it orders nothing. Data hand-offs use
+// mbar_arrive_remote_release.
 ISB_DEVICE void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+
+// Release remote arrive: publishes this thread's prior shared-memory writes (and
+// those ordered before it by a CTA barrier) to the peer that acquires the phase
+// (mbar_wait_cluster). Used for "partials ready" hand-offs read over DSMEM.
+ISB_DEVICE void mbar_arrive_remote_release(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
 

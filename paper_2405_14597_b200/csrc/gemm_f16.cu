@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(DCfg<MT>::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&d_empty[buf]);
-        if (lane < static_cast<uint32_t>(p.C)) mbar_arrive_remote(mapa_shared(smem_u32(red_full), lane));
+        if (lane < static_cast<uint32_t>(p.C)) mbar_arrive_remote_release(mapa_shared(smem_u32(red_full), lane));
         mbar_wait_cluster(red_full, it & 1);
         const int lo = rank * MT / p.C, hi = (rank + 1) * MT / p.C;
         for (int t = lo; t < hi; ++t) {

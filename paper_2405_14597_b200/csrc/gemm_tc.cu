@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
         mbar_wait(&pb_full[buf], ph);
         if (p.C > 1) {
           if (lane < static_cast<uint32_t>(p.C))
-            mbar_arrive_remote(mapa_shared(smem_u32(&red_full[buf]), lane));
+            mbar_arrive_remote_release(mapa_shared(smem_u32(&red_full[buf]), lane));
           mbar_wait_cluster(&red_full[buf], ph);
         }
         if (warp == 2 && lane == 0) ISB_TRACE(6, it);

@@ -21,10 +21,13 @@ static __device__ __noinline__ float quant_exact(float xf, double s) {
 }
 
 __device__ __forceinline__ int quant_one(float xf, double s, double r, int qmin, int qmax) {
-  const float y = xf * static_cast<float>(r);
+  const float rf = static_cast<float>(r);
+  const float y = xf * rf;
   const float ay = fabsf(y);
   float q = rintf(y);  // not near a tie: nearest integer == round half away from zero
-  if (fabsf((ay - floorf(ay)) - 0.5f) <= 1e-3f) q = quant_exact(xf, s);
+  // Rows with absmax below ~127/FLT_MAX make fl32(1/s) infinite: the exact path
+  // decides every element of such a row (the comparison is false for inf/NaN).
+  if (!(fabsf((ay - floorf(ay)) - 0.5f) > 1e-3f) || !(rf <= 3.4e38f)) q = quant_exact(xf, s);
   q = fminf(fmaxf(q, static_cast<float>(qmin)), static_cast<float>(qmax));
   return static_cast<int>(q);
 }

@@ -328,7 +328,12 @@ def gemm_act_fused(x, w: PackedWeight, path: str = "integer-scale", out_dtype=to
         out = torch.empty((m, w.n), dtype=out_dtype, device=x.device)
     if sa_out is not None:
         sa_out = _cuda(sa_out, torch.float64)
-    ws, need = _ws_for(m, w, workspace)
+    b = C.c_int64()
+    check(load().isb_gemm_act_fused_workspace_size(m, w.handle, C.byref(b)))
+    if workspace is None:
+        key = (w.device, torch.cuda.current_stream(w.device).cuda_stream)
+        workspace = _default_ws.setdefault(key, Workspace())
+    ws = workspace.get(b.value, w.device)
     p = ISB_PATH_INTEGER_SCALE if path == "integer-scale" else ISB_PATH_FLOAT_SCALE
     check(load().isb_gemm_act_fused(p, _ptr(x), _DT[x.dtype], m, k, w.handle, _ptr(out),
                                     _DT[out.dtype], _ptr(sa_out), _ptr(ws), ws.numel(),

@@ -57,6 +57,29 @@ def column_shard(codes, scales, int_scales, rank: int, world: int):
     return codes[:, n0:n1], scales[n0 * g_count:n1 * g_count], ks, (n0, n1)
 
 
+def static_bound(int_scales, groups: int, group: int, act_bits=8, w_bits=4) -> int:
+    """overflow_analyzer's bound (analysis.cpp:24-59): max over output channels of
+    sum_g group * A_max * W_max * k_g, in exact Python integers."""
+    if isinstance(int_scales, torch.Tensor):
+        int_scales = int_scales.detach().cpu().numpy()
+    ks = np.asarray(int_scales, np.int64).reshape(-1, groups)
+    per_mac = group * ((1 << (act_bits - 1)) - 1) * (1 << (w_bits - 1))
+    return int(max(int(v) for v in ks.sum(axis=1))) * per_mac if ks.size else 0
+
+
+def require_int32_safe(int_scales, groups: int, group: int, what: str):
+    """The int32 all-reduce of row-parallel partial accumulators equals the
+    reference's int64 acc only if the WHOLE layer's static bound fits int32 (each
+    shard's bound is smaller, so the per-rank kernels' own gate is not enough)."""
+    b = static_bound(int_scales, groups, group)
+    if b > (1 << 31) - 1:
+        from ._lib import OverflowError_
+        raise OverflowError_(f"{what}: static overflow bound {b} exceeds int32 "
+                             "(analysis.cpp:24-59); the int32 accumulator exchange "
+                             "would not be exact")
+    return b
+
+
 def row_shard(codes, scales, int_scales, group: int, rank: int, world: int):
     """Quantization groups [g0, g1) of a K x N weight (K split on group boundaries):
     codes rows [g0 g, g1 g) and, per output channel c, units c*G + [g0, g1)."""
@@ -181,6 +204,7 @@ class RowParallelLinear:
 
     def __init__(self, codes, scales, int_scales, amplifier: int, group: int, comm: Comm,
                  backend):
+        require_int32_safe(int_scales, codes.shape[0] // group, group, "RowParallelLinear")
         c, s, ks, (g0, g1) = row_shard(codes, scales, int_scales, group, comm.rank, comm.world)
         self.comm, self.backend, self.amplifier, self.group = comm, backend, amplifier, group
         self.shard = ShardInfo(g0 * group, g1 * group, [])

@@ -193,3 +193,26 @@ def test_tensor_parallel_shards_on_device_bit_exact(world, m, k, n):
     out_bf = be.finalize(acc, sa_full, s.amplifier, torch.bfloat16).float().cpu().numpy()
     assert np.array_equal(out_bf, torch.from_numpy(ref).to(torch.bfloat16).float().numpy())
     assert isb.launch_count() > 0
+
+
+def test_row_parallel_refuses_unsafe_layer():
+    """The int32 all-reduce is exact only under the WHOLE layer's static bound
+    (analysis.cpp:24-59): LLaMA-2-70B down_proj-like K=28672 at alpha=8192 style
+    scales (k_g ~ 124) is unsafe although each 1/8 shard alone would be safe."""
+    P = par
+    from paper_2405_14597_b200._lib import OverflowError_
+    k, n, g = 28672, 4, 128
+    groups = k // g
+    ks = np.full(n * groups, 124, np.int32)
+    bound = P.static_bound(ks, groups, g)
+    assert bound == groups * 128 * 127 * 8 * 124 and bound > 2**31 - 1
+    assert P.static_bound(ks.reshape(n, groups)[:, : groups // 8].ravel(), groups // 8, g) < 2**31
+    ref = O.overflow_analyzer(k, g, 8, 4, O.IntegerScaleSet(ks, 8192, 13))
+    assert ref["static_bound"] == bound and not ref["safe"]
+
+    class _Comm:
+        rank, world = 0, 8
+
+    with pytest.raises(OverflowError_):
+        P.RowParallelLinear(np.zeros((k, n), np.int16), np.full(n * groups, 1e-3), ks, 8192, g,
+                            _Comm(), OracleBackend())
