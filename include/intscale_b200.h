@@ -157,6 +157,50 @@ int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t 
 int isb_gemm_act_fused_workspace_size(int64_t m, const isb_weight* w, int64_t* bytes);
 
 /* --------------------------------------------------------------------------
+ * Grouped layer launch — K1 (+) K3/K4 for up to ISB_GROUP_MAX_PROBLEMS GEMMs in
+ * ONE persistent kernel (the linears of a decoder layer that share an input
+ * step, or the experts of a MoE layer). Per problem p the result is exactly
+ * quantize(x_p, 8, symmetric, per_token) (quantize.cpp:93-145) followed by
+ * gemm_integer_scale (gemm.cpp:205-262) or gemm_float_scale (gemm.cpp:156-203)
+ * — bit-identical to isb_quantize_per_token + isb_gemm_integer_scale /
+ * isb_gemm_float_scale on the same inputs.
+ *  - x != NULL (every problem): float32 / bf16 activations [m][k], quantized
+ *    inside the launch; xq / sa (nullable) receive the codes and scales (the
+ *    plan owns buffers for the NULL ones).
+ *  - x == NULL (every problem): xq / sa are the int8 codes and double scales.
+ *  - m may differ per problem (0 = no work: an expert with no routed token).
+ *  - weights: group == 128, K % 128 == 0; integer path: overflow_analyzer
+ *    bound within int32, else ISB_OVERFLOW (as isb_gemm_integer_scale).
+ * The plan binds every pointer at creation (it allocates its schedule, counters
+ * and any owned buffers there, never in isb_group_run) and may be replayed any
+ * number of times, including inside CUDA graphs; one run at a time per plan.
+ * Non-finite activations raise a sticky device flag, read (synchronously) with
+ * isb_group_nonfinite — the in-launch analogue of isb_quantize_per_token's
+ * check_finite.
+ */
+#define ISB_GROUP_MAX_PROBLEMS 8
+typedef struct {
+  const isb_weight* w;
+  int64_t m;
+  const void* x;   /* float32 / bf16 [m][k] or NULL */
+  int32_t x_dtype; /* ISB_F32 / ISB_BF16 */
+  int8_t* xq;      /* int8 codes [m][k] */
+  double* sa;      /* token scales [m] */
+  void* out;       /* [m][n] out_dtype */
+} isb_group_problem;
+typedef struct {
+  int32_t grid, cluster, tile_tokens, quantize;
+  double makespan_steps; /* planner's per-cluster makespan (steps of 4 x 8 KiB) */
+} isb_group_info_t;
+typedef struct isb_group_plan isb_group_plan;
+int isb_group_plan_create(const isb_group_problem* problems, int32_t nprob, int32_t path,
+                          int32_t out_dtype, isb_group_plan** plan);
+int isb_group_run(isb_group_plan* plan, void* stream);
+int isb_group_plan_info(const isb_group_plan* plan, isb_group_info_t* info);
+int isb_group_nonfinite(isb_group_plan* plan, int32_t clear, int32_t* raised);
+int isb_group_plan_destroy(isb_group_plan* plan);
+
+/* --------------------------------------------------------------------------
  * Dense fp16 / bf16 baseline GEMM (no reference analogue; BASELINE.json north
  * star: "an fp16 cuBLAS-free dense baseline kernel ... reported for the paper's
  * speedup claims"): out[M][N] = x[M][K] * w[N][K]^T (nn.Linear weight layout),

@@ -8,7 +8,7 @@ libintscale_b200.so (hand-written CUDA for sm_100a) behind a C ABI.
 """
 from ._lib import (CudaError, DimensionError, FormatError, IntscaleError, LengthError,  # noqa
                    OverflowError_, ParamError, ValueError_)
-from .ops import (IntegerScaleSet, PackedWeight, Workspace, finalize_acc,  # noqa: F401
+from .ops import (GroupedGemm, IntegerScaleSet, PackedWeight, Workspace, finalize_acc,  # noqa: F401
                   DualInner, dual_inner_quantize, gemm_dual_quant,
                   gemm_act_fused, gemm_checked, gemm_coarse, gemm_dense, gemm_float_scale, gemm_integer_scale,
                   integerize_scales, launch_count, overflow_analyzer, quantize_per_token,

@@ -66,6 +66,16 @@ class WeightInfo(C.Structure):
     ]
 
 
+class GroupProblem(C.Structure):
+    _fields_ = [("w", C.c_void_p), ("m", C.c_int64), ("x", C.c_void_p), ("x_dtype", C.c_int32),
+                ("xq", C.c_void_p), ("sa", C.c_void_p), ("out", C.c_void_p)]
+
+
+class GroupInfo(C.Structure):
+    _fields_ = [("grid", C.c_int32), ("cluster", C.c_int32), ("tile_tokens", C.c_int32),
+                ("quantize", C.c_int32), ("makespan_steps", C.c_double)]
+
+
 class GemmStats(C.Structure):
     _fields_ = [
         ("max_abs_accumulator", C.c_int64), ("overflow_detected", C.c_int32),
@@ -107,6 +117,12 @@ SIGNATURES = {
     "isb_gemm_dual_quant": (_INT, [_VP, _VP, _I64, _I64, _VP, _VP, _VP, _I64, _VP, _I64, _VP, _VP,
                                     _VP]),
     "isb_gemm_dense": (_INT, [_VP, _VP, _INT, _I64, _I64, _I64, _VP, _INT, _VP]),
+    "isb_group_plan_create": (_INT, [C.POINTER(GroupProblem), _I32, _I32, _I32,
+                                     C.POINTER(_VP)]),
+    "isb_group_run": (_INT, [_VP, _VP]),
+    "isb_group_plan_info": (_INT, [_VP, C.POINTER(GroupInfo)]),
+    "isb_group_nonfinite": (_INT, [_VP, _I32, C.POINTER(_I32)]),
+    "isb_group_plan_destroy": (_INT, [_VP]),
     "isb_row_absmax": (_INT, [_VP, _INT, _I64, _I64, _VP, _VP]),
     "isb_quantize_per_token_amax": (_INT, [_VP, _INT, _I64, _I64, _VP, _VP, _VP, _VP]),
 }

@@ -474,6 +474,41 @@ int isb_gemm_act_fused_workspace_size(int64_t m, const isb_weight* w, int64_t* b
   });
 }
 
+int isb_group_plan_create(const isb_group_problem* problems, int32_t nprob, int32_t path,
+                          int32_t out_dtype, isb_group_plan** plan) {
+  return guarded([&] {
+    if (!plan) fail(ISB_PARAM, "null plan pointer");
+    if (!problems) fail(ISB_PARAM, "null problem list");
+    *plan = reinterpret_cast<isb_group_plan*>(
+        group_plan_create(problems, nprob, path, out_dtype, num_sms()));
+  });
+}
+
+int isb_group_run(isb_group_plan* plan, void* stream) {
+  return guarded([&] {
+    if (!plan) fail(ISB_PARAM, "null plan");
+    group_plan_run(reinterpret_cast<GroupPlan*>(plan), as_stream(stream));
+  });
+}
+
+int isb_group_plan_info(const isb_group_plan* plan, isb_group_info_t* info) {
+  return guarded([&] {
+    if (!plan || !info) fail(ISB_PARAM, "null argument");
+    group_plan_info(reinterpret_cast<const GroupPlan*>(plan), info);
+  });
+}
+
+int isb_group_nonfinite(isb_group_plan* plan, int32_t clear, int32_t* raised) {
+  return guarded([&] {
+    if (!plan || !raised) fail(ISB_PARAM, "null argument");
+    *raised = group_plan_nonfinite(reinterpret_cast<GroupPlan*>(plan), clear != 0);
+  });
+}
+
+int isb_group_plan_destroy(isb_group_plan* plan) {
+  return guarded([&] { group_plan_destroy(reinterpret_cast<GroupPlan*>(plan)); });
+}
+
 int isb_gemm_dense(const void* x, const void* w, int dtype, int64_t m, int64_t n, int64_t k,
                    void* out, int out_dtype, void* stream) {
   return guarded([&] {

@@ -114,6 +114,14 @@ void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, con
                     void* out, int out_dtype, void* workspace, const GemmPlan& plan,
                     cudaStream_t s, const void* xf = nullptr, int x_dtype = 0,
                     double* sa_out = nullptr);
+// Grouped layer launch (gemm_group.cu).
+struct GroupPlan;
+GroupPlan* group_plan_create(const isb_group_problem* probs, int nprob, int path, int out_dtype,
+                             int num_sms);
+void group_plan_run(GroupPlan* pl, cudaStream_t s);
+void group_plan_info(const GroupPlan* pl, isb_group_info_t* info);
+int group_plan_nonfinite(GroupPlan* pl, bool clear);
+void group_plan_destroy(GroupPlan* pl);
 void launch_gemm_checked(int path, const int8_t* xq, const double* sa, int64_t m,
                          const isb_weight& w, float* out, double* out_f64, int64_t* acc,
                          int64_t* partials, unsigned long long* stats_dev, cudaStream_t s);

@@ -14,7 +14,8 @@ import torch
 
 from . import _lib
 from ._lib import (ISB_BF16, ISB_F16, ISB_F32, ISB_I32, ISB_PATH_FLOAT_SCALE,
-                   ISB_PATH_INTEGER_SCALE, GemmStats, WeightInfo, check, load)
+                   ISB_PATH_INTEGER_SCALE, GemmStats, GroupInfo, GroupProblem, WeightInfo, check,
+                   load)
 
 _DT = {torch.float32: ISB_F32, torch.bfloat16: ISB_BF16, torch.float16: ISB_F16,
        torch.int32: ISB_I32}
@@ -339,6 +340,88 @@ def gemm_act_fused(x, w: PackedWeight, path: str = "integer-scale", out_dtype=to
                                     _DT[out.dtype], _ptr(sa_out), _ptr(ws), ws.numel(),
                                     _stream(stream)))
     return out
+
+
+class GroupedGemm:
+    """Grouped layer launch (isb_group_plan_*): up to 8 W4A8 GEMMs — e.g. the
+    linears of one decoder layer, or the experts of a MoE layer — in ONE
+    persistent tcgen05 launch, per-token activation quantization (K1) included.
+    Per problem the output is bit-identical to quantize_per_token followed by
+    gemm_integer_scale / gemm_float_scale.
+
+    problems: sequence of dicts with
+      weight  PackedWeight (group 128)
+      x       float32 / bf16 [M, K] activations (quantized in the launch), or
+      xq, sa  int8 codes [M, K] and float64 scales [M] (pre-quantized), and
+      out     optional preallocated [M, N] output (else allocated here).
+    With `x`, `xq` / `sa` may be given to receive the codes and scales.
+    Every pointer is bound at construction: run() replays the launch (CUDA-graph
+    safe); keep the tensors alive and update them in place."""
+
+    def __init__(self, problems, path: str = "integer-scale", out_dtype=torch.bfloat16):
+        if not 1 <= len(problems) <= 8:
+            raise _lib.ParamError("grouped GEMM: 1..8 problems")
+        arr = (GroupProblem * len(problems))()
+        self.outs, self._keep = [], []
+        for i, pr in enumerate(problems):
+            w = pr["weight"]
+            x, xq, sa = pr.get("x"), pr.get("xq"), pr.get("sa")
+            if x is not None:
+                x = _cuda(x)
+                if x.dtype not in (torch.float32, torch.bfloat16) or x.dim() != 2:
+                    raise _lib.ParamError("activations must be 2-d float32 or bfloat16")
+                m, k = x.shape
+                if xq is not None:
+                    xq = _cuda(xq, torch.int8)
+                if sa is not None:
+                    sa = _cuda(sa, torch.float64)
+            else:
+                xq, sa = _cuda(xq, torch.int8), _cuda(sa, torch.float64)
+                m, k = xq.shape
+            if k != w.k:
+                raise _lib.DimensionError(f"activation K={k} vs weight rows {w.k}")
+            out = pr.get("out")
+            if out is None:
+                out = torch.empty((m, w.n), dtype=out_dtype, device=w.device)
+            elif out.dtype != out_dtype or tuple(out.shape) != (m, w.n):
+                raise _lib.ParamError("output tensor shape / dtype mismatch")
+            arr[i] = GroupProblem(w.handle.value, m, None if x is None else x.data_ptr(),
+                                  _DT[x.dtype] if x is not None else 0,
+                                  None if xq is None else xq.data_ptr(),
+                                  None if sa is None else sa.data_ptr(), out.data_ptr())
+            self.outs.append(out)
+            self._keep += [w, x, xq, sa, out]
+        self.path = ISB_PATH_INTEGER_SCALE if path == "integer-scale" else ISB_PATH_FLOAT_SCALE
+        h = C.c_void_p()
+        check(load().isb_group_plan_create(arr, len(problems), self.path, _DT[out_dtype],
+                                           C.byref(h)))
+        self._h = h
+        info = GroupInfo()
+        check(load().isb_group_plan_info(h, C.byref(info)))
+        self.grid, self.cluster, self.tile_tokens = info.grid, info.cluster, info.tile_tokens
+        self.makespan_steps = info.makespan_steps
+
+    def run(self, stream=None):
+        check(load().isb_group_run(self._h, _stream(stream)))
+        return self.outs
+
+    def nonfinite(self, clear: bool = True) -> bool:
+        """Whether any activation quantized by this plan was non-finite (synchronous;
+        the reference quantizer's ValueError, quantize.cpp)."""
+        r = C.c_int32()
+        check(load().isb_group_nonfinite(self._h, 1 if clear else 0, C.byref(r)))
+        return bool(r.value)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load().isb_group_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def gemm_checked(path: str, xq, sa, w: PackedWeight, strict=False, want_f64=True, want_acc=True,

@@ -1,0 +1,236 @@
+"""Grouped layer launch (isb_group_plan_*, csrc/gemm_group.cu) parity.
+
+Per problem the grouped launch must equal quantize(x, 8, symmetric, per_token)
+(quantize.cpp:93-145) followed by gemm_integer_scale (gemm.cpp:205-262) bit for
+bit — checked against the oracle on small shapes and, at the LLaMA / Mixtral
+sizes, against K1 + the single-GEMM kernel (itself oracle-checked in
+test_gpu_parity.py / test_gpu_scale.py). Float scale (gemm.cpp:156-203): within
+the fp32-accumulation bound. Replays (CUDA graph, >= 50) must be identical: the
+in-kernel readiness counters re-arm themselves at the end of every launch.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU, skipped there
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2405_14597_b200 as isb  # noqa: E402
+
+DEV = torch.device("cuda:0")
+LLAMA2_7B = [(4096, 12288), (4096, 4096), (4096, 22016), (11008, 4096)]
+
+
+def dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(DEV)
+
+
+def device_weight(k, n, seed, amp=1024):
+    """llama_like weight quantized on the device (bit-exact group quantizer)."""
+    from bench import llama_like_weight
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(seed)
+    wf = llama_like_weight(k, n, gen, DEV)
+    codes, scales = isb.quantize_weight(wf, 128, 4)
+    si = isb.integerize_scales(scales.cpu().numpy(), amp)
+    return isb.PackedWeight.from_codes(codes, 128, scales, si.int_scales, amp)
+
+
+_W = {}
+
+
+def layer_weights(shapes, tag=0):
+    key = (tuple(shapes), tag)
+    if key not in _W:
+        _W[key] = [device_weight(k, n, seed=11 * k + n + tag) for k, n in shapes]
+    return _W[key]
+
+
+def single_reference(x, w, path, out_dtype):
+    q, sa = isb.quantize_per_token(x)
+    f = isb.gemm_integer_scale if path == "integer-scale" else isb.gemm_float_scale
+    return q, sa, f(q, sa, w, out_dtype=out_dtype)
+
+
+@pytest.mark.parametrize("m", [1, 3, 16, 17, 32, 64])
+def test_group_layer_matches_k1_plus_k3(m):
+    ws = layer_weights(LLAMA2_7B)
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(100 + m)
+    xs = [torch.randn((m, k), generator=gen, device=DEV) * (1 + i) for i, (k, _) in
+          enumerate(LLAMA2_7B)]
+    codes = [torch.empty((m, k), dtype=torch.int8, device=DEV) for k, _ in LLAMA2_7B]
+    scales = [torch.empty((m,), dtype=torch.float64, device=DEV) for _ in LLAMA2_7B]
+    g = isb.GroupedGemm([{"weight": w, "x": x, "xq": c, "sa": s}
+                         for w, x, c, s in zip(ws, xs, codes, scales)])
+    outs = g.run()
+    torch.cuda.synchronize()
+    for i, (x, w) in enumerate(zip(xs, ws)):
+        q, sa, ref = single_reference(x, w, "integer-scale", torch.bfloat16)
+        assert torch.equal(codes[i], q), f"codes differ (problem {i})"
+        assert torch.equal(scales[i], sa), f"scales differ (problem {i})"
+        assert torch.equal(outs[i], ref), f"output differs (problem {i}, m={m})"
+    assert not g.nonfinite()
+
+
+def test_group_small_vs_oracle_all_dtypes():
+    """Oracle directly: two problems of different K/N/M, float32 activations."""
+    shapes = [(3, 512, 384), (5, 1024, 256)]
+    probs, refs = [], []
+    for i, (m, k, n) in enumerate(shapes):
+        wf = O.generate_llama_like(k, n, 40 + i)
+        xf = O.generate_gaussian(m, k, 1.0, 50 + i)
+        wo = O.quantize_weight(wf, 128)
+        so = O.integerize_scales(wo.scales, 1024)
+        xo = O.quantize_per_token(xf)
+        refs.append((xo, O.gemm_integer_scale(xo, wo, so), O.gemm_float_scale(xo, wo)))
+        w = isb.PackedWeight.from_codes(dev(wo.values), 128, dev(wo.scales), dev(so.int_scales),
+                                        so.amplifier)
+        probs.append((w, dev(xf)))
+    for dt in (torch.float32, torch.bfloat16, torch.int32):
+        g = isb.GroupedGemm([{"weight": w, "x": x} for w, x in probs], out_dtype=dt)
+        outs = [o.clone() for o in g.run()]
+        torch.cuda.synchronize()
+        for (xo, ri, _), o in zip(refs, outs):
+            if dt == torch.int32:
+                assert np.array_equal(o.cpu().numpy().astype(np.int64), ri.acc)
+            elif dt == torch.float32:
+                assert np.array_equal(o.cpu().numpy().view(np.int32), ri.output.view(np.int32))
+            else:
+                assert torch.equal(o.cpu(), torch.from_numpy(ri.output).to(torch.bfloat16))
+    g = isb.GroupedGemm([{"weight": w, "x": x} for w, x in probs], path="float-scale",
+                        out_dtype=torch.float32)
+    outs = g.run()
+    torch.cuda.synchronize()
+    for (xo, _, rf), o in zip(refs, outs):
+        err = np.abs(o.cpu().numpy().astype(np.float64) - rf.output_f64).max()
+        assert err <= 1e-5 * np.abs(rf.output_f64).max()
+
+
+def test_group_prequantized_inputs():
+    m = 16
+    ws = layer_weights(LLAMA2_7B)
+    xq = [isb.quantize_per_token(torch.randn((m, k), device=DEV)) for k, _ in LLAMA2_7B]
+    g = isb.GroupedGemm([{"weight": w, "xq": q, "sa": s} for w, (q, s) in zip(ws, xq)])
+    outs = g.run()
+    for (q, s), w, o in zip(xq, ws, outs):
+        assert torch.equal(o, isb.gemm_integer_scale(q, s, w))
+
+
+def test_group_graph_replay_is_stable_and_tracks_inputs():
+    """50 graph replays of the quantizing launch give identical results (the
+    readiness counters re-arm); changing the activations in place between replays
+    changes the result exactly as K1 + K3 does."""
+    m = 16
+    ws = layer_weights(LLAMA2_7B)
+    xs = [torch.randn((m, k), device=DEV) for k, _ in LLAMA2_7B]
+    g = isb.GroupedGemm([{"weight": w, "x": x} for w, x in zip(ws, xs)])
+    g.run()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            g.run()
+    torch.cuda.current_stream().wait_stream(s)
+    graph.replay()
+    torch.cuda.synchronize()
+    first = [o.clone() for o in g.outs]
+    bad = torch.zeros((), dtype=torch.int64, device=DEV)
+    for _ in range(50):
+        graph.replay()
+        for o, f in zip(g.outs, first):
+            bad += (o != f).sum()
+    torch.cuda.synchronize()
+    assert int(bad) == 0
+    for i, (x, w) in enumerate(zip(xs, ws)):
+        assert torch.equal(first[i], single_reference(x, w, "integer-scale", torch.bfloat16)[2])
+    for x in xs:
+        x.mul_(-0.5).add_(0.25)
+    graph.replay()
+    torch.cuda.synchronize()
+    for i, (x, w) in enumerate(zip(xs, ws)):
+        assert torch.equal(g.outs[i], single_reference(x, w, "integer-scale", torch.bfloat16)[2])
+
+
+def test_group_moe_experts_ragged_rows():
+    """Mixtral-8x7B w1|w3 experts (4096 -> 2 x 14336) with ragged routed rows,
+    including an expert with no tokens; bf16 activations."""
+    counts = [5, 0, 3, 1, 9, 2, 4, 8]
+    w = layer_weights([(4096, 28672)], tag=7)[0]
+    xs = [torch.randn((c, 4096), device=DEV).to(torch.bfloat16) for c in counts]
+    g = isb.GroupedGemm([{"weight": w, "x": x} for x in xs], out_dtype=torch.float32)
+    outs = g.run()
+    torch.cuda.synchronize()
+    for x, o in zip(xs, outs):
+        if x.shape[0] == 0:
+            assert o.shape == (0, 28672)
+            continue
+        assert torch.equal(o, single_reference(x, w, "integer-scale", torch.float32)[2])
+
+
+def test_group_float_scale_within_bound():
+    m = 16
+    ws = layer_weights(LLAMA2_7B)
+    xs = [torch.randn((m, k), device=DEV) for k, _ in LLAMA2_7B]
+    g = isb.GroupedGemm([{"weight": w, "x": x} for w, x in zip(ws, xs)], path="float-scale",
+                        out_dtype=torch.float32)
+    outs = g.run()
+    for x, w, o in zip(xs, ws, outs):
+        ref = single_reference(x, w, "float-scale", torch.float32)[2].double()
+        tol = 1e-5 * ref.abs().max()
+        assert float((o.double() - ref).abs().max()) <= float(tol)
+
+
+def test_group_forced_split_widths():
+    """Every split-K width the planner may pick gives the same exact result."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, torch
+sys.path.insert(0, %r)
+import paper_2405_14597_b200 as isb
+from tests.test_gpu_group import layer_weights, single_reference, LLAMA2_7B, DEV
+for m in (1, 16, 40):
+    ws = layer_weights(LLAMA2_7B)
+    xs = [torch.randn((m, k), device=DEV) for k, _ in LLAMA2_7B]
+    g = isb.GroupedGemm([{"weight": w, "x": x} for w, x in zip(ws, xs)])
+    for _ in range(20):
+        g.run()
+    torch.cuda.synchronize()
+    for x, w, o in zip(xs, ws, g.outs):
+        assert torch.equal(o, single_reference(x, w, "integer-scale", torch.bfloat16)[2]), (m, g.cluster)
+print("ok", g.cluster)
+""" % root
+    for c in ("1", "2", "4", "8"):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                           env=dict(os.environ, ISB_GROUP_C=c), timeout=600)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-1500:] + r.stderr[-3000:]
+        assert r.stdout.split()[-1] == c
+
+
+def test_group_refuses_unsafe_layer_and_flags_nonfinite():
+    from tests.instances import overflow_rig
+    x, w, s = overflow_rig(16)
+    pw = isb.PackedWeight.from_codes(dev(w.values), w.group, dev(w.scales), dev(s.int_scales),
+                                     s.amplifier)
+    with pytest.raises(isb.OverflowError_):
+        isb.GroupedGemm([{"weight": pw, "x": torch.ones((1, 4096), device=DEV)}])
+    ws = layer_weights(LLAMA2_7B)
+    xs = [torch.randn((4, k), device=DEV) for k, _ in LLAMA2_7B]
+    xs[2][1, 7] = float("nan")
+    g = isb.GroupedGemm([{"weight": w, "x": x} for w, x in zip(ws, xs)])
+    g.run()
+    assert g.nonfinite()
+    assert not g.nonfinite()  # cleared
