@@ -28,7 +28,7 @@ ISB_DEVICE int64_t clock64_() {
 
 ISB_DEVICE int64_t globaltimer_() {
   int64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
   return t;
 }
 

@@ -12,33 +12,45 @@
 // first-byte latency, split-K tail) that the weight stream cannot hide, and the
 // K1 launches in front of each GEMM are pure latency. Here the SMs
 // stream the weights of all problems back to back; the tiles of all problems
-// are scheduled over the clusters longest-first (host LPT), so the tail is paid
-// once per layer instead of once per GEMM.
+// are spread evenly over the SMs (below), so the tail is paid once per layer
+// instead of once per GEMM.
 //
 // Per CTA the pipeline is the single-GEMM decode pipeline (gemm_tc.cu): producer
 // warp (bulk copy of packed int4 weights + int32 k_g, TMA of int8 activation
 // tiles), two transform warpgroups (int4 -> TMEM int8), MMA warp
 // (tcgen05.mma.kind::i8, TMEM accumulators), epilogue warpgroup (per-group
-// IMAD / FFMA), two reduction warps (cluster split-K over DSMEM + Eq. 2). What
-// differs is the work list (a per-cluster schedule of (problem, tile) entries)
-// and the activation hand-off:
+// IMAD / FFMA), two reduction warps (Eq. 2 and the output stores). What differs:
 //
-//   quantize phase  the epilogue warpgroup of CTA b quantizes token rows b,
-//                   b + grid, ... of the concatenated problems (exact K1
-//                   arithmetic, quant.cuh) into the problem's int8 code buffer
-//                   and double scales, then publishes the row with a
-//                   gpu-scope release add on the problem's readiness counter;
+//   schedule        one CTA per SM, no clusters. The host lays the (problem,
+//                   tile) work out McNaughton-style: tiles are poured in order
+//                   into per-CTA budgets of equal length, a tile that crosses a
+//                   budget boundary continues on the next CTA. Every CTA gets
+//                   the same number of 128-K blocks (+- one block), whatever
+//                   the mix of K over the problems, and at most one tile per
+//                   CTA boundary is split. A tile split into pieces is reduced
+//                   through global memory in fixed piece order: each piece
+//                   stores its partial (int32 or fp32) to its own slot, counts
+//                   itself in with an acq_rel add, and the piece that completes
+//                   the count sums the slots 0..n-1 and applies the epilogue —
+//                   deterministic, and exact on the integer path;
+//   quantize phase  CTA b quantizes token rows b, b + grid, ... of the
+//                   concatenated problems (all its threads, exact K1 arithmetic,
+//                   quant.cuh) into the problem's int8 code buffer and double
+//                   scales, then publishes the row with a gpu-scope release add
+//                   on the problem's readiness counter;
 //   consumers       the producer (before the first TMA of a problem's codes)
 //                   and the reduction warps (before reading its token scales)
-//                   acquire-poll the counter until all M rows are in. The weight
-//                   stream never waits: the first kStages steps are in flight
-//                   before griddepcontrol.wait, and weight loads of later steps
-//                   are issued ahead of the activation loads.
-//   reset           the last CTA to retire (acq_rel counter) zeroes the
-//                   counters, so the plan can be replayed (CUDA graphs) with no
-//                   memset node. All CTAs are co-resident (grid <= the
-//                   occupancy-derived cluster capacity), so the polls cannot
-//                   deadlock.
+//                   acquire-poll the counter until all M rows are in. The first
+//                   kStages weight steps are in flight before
+//                   griddepcontrol.wait;
+//   replays         the readiness counters are cumulative; each CTA takes a
+//                   ticket (64-bit atomic) before the launch triggers its
+//                   dependents, and ticket / grid is the launch epoch the
+//                   waits are relative to; every split finisher zeroes its own
+//                   counter. A plan replays (CUDA graphs) with no memset node
+//                   and no end-of-kernel atomic. All CTAs are co-resident
+//                   (grid <= the occupancy-derived capacity), so the polls
+//                   cannot deadlock.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -62,9 +74,9 @@ namespace isb {
 namespace {
 
 constexpr int kMaxGroup = ISB_GROUP_MAX_PROBLEMS;
-constexpr int kSyncDone = kMaxGroup;      // CTAs retired
-constexpr int kSyncBad = kMaxGroup + 1;   // non-finite activation seen (sticky)
-constexpr int kSyncWords = kMaxGroup + 2;
+constexpr int kSyncTicket = kMaxGroup;    // 64-bit CTA ticket counter (launch epoch)
+constexpr int kSyncBad = kMaxGroup + 2;   // non-finite activation seen (sticky)
+constexpr int kSyncWords = kMaxGroup + 4;
 
 struct GProb {
   const uint8_t* packed;
@@ -83,10 +95,20 @@ struct GProb {
 struct GParams {
   GProb prob[kMaxGroup];
   int qoff[kMaxGroup + 1];  // prefix sums of M over problems (quantize row tasks)
-  int nprob, C, NC, quantize, qtasks, sched_stride;
-  const int* sched;         // [NC][sched_stride]: (problem << 24) | tile
+  int nprob, NC, quantize, qtasks, sched_stride;
+  const int4* sched;        // [NC][sched_stride] pieces: {p << 24 | tile, g0 << 16 | g1,
+                            //  piece << 16 | npieces, split id (-1: whole tile)}
   const int* sched_len;     // [NC]
-  unsigned* sync;           // [kSyncWords]
+  const int* split_base;    // [nsplit] first partial slot of each split tile
+  uint32_t* partials;       // [slots][MT][128] int32 / fp32 piece partials
+  unsigned* sync;           // [kSyncWords] + [nsplit] split-tile piece counters
+  int dbg;                  // measurement knobs (isb_debug_set_flags): 1 skip TMEM st,
+                            // 2 skip TMEM ld, 4 skip MMA, 8 skip the activation wait,
+                            // 16 no weight prefetch before the quantize phase,
+                            // 32 launch-overhead probe (no work), 64 no activation
+                            // TMA, 128 no scale loads, 256 no output / reduction,
+                            
+  int64_t* trace;           // optional per-CTA timeline [4][512] (isb_debug_set_trace)
 };
 
 struct alignas(64) GMaps {
@@ -114,36 +136,38 @@ ISB_DEVICE void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Spin (with back-off) until all `target` rows of a problem are published.
-ISB_DEVICE void wait_rows(const unsigned* ctr, unsigned target) {
-  while (ld_acquire_gpu(ctr) < target) __nanosleep(32);
+// Spin (with back-off) until all `rows` rows of a problem are published in this
+// launch. The counters are cumulative over launches: launch `epoch` waits for
+// epoch * rows + rows (modulo 2^32).
+ISB_DEVICE void wait_rows(const unsigned* ctr, unsigned epoch, unsigned rows) {
+  const unsigned base = epoch * rows;
+  while (ld_acquire_gpu(ctr) - base < rows) __nanosleep(32);
 }
 
-// The CTA's walk over its cluster's schedule, one step (S 128-K blocks of one
-// tile) at a time. Rank q of the cluster owns groups [q G / C, (q+1) G / C) of
-// every tile (g = 128: one group per 128-K block).
+// The CTA's walk over its pieces, one step (S 128-K blocks = S groups of one
+// piece) at a time.
 template <int S>
 struct GCur {
-  const GParams* P;
-  int cid, rank, it, ntiles, sj, nst, pi, nt, mt, kb0, kb1;
-  __device__ void init(const GParams& prm, int cid_, int rank_) {
-    P = &prm;
-    cid = cid_;
-    rank = rank_;
+  const GProb* probs;
+  const int4* list;
+  int it, ntiles, sj, nst, pi, nt, mt, kb0, kb1;
+  __device__ void init(const GProb* probs_, const int4* list_, int ntiles_) {
+    probs = probs_;
+    list = list_;
+    ntiles = ntiles_;
     it = 0;
     sj = 0;
-    ntiles = cid < prm.NC ? prm.sched_len[cid] : 0;
     if (ntiles > 0) load();
   }
   __device__ void load() {
-    const int e = P->sched[cid * P->sched_stride + it];
-    pi = e >> 24;
-    const int t = e & 0xFFFFFF;
-    const GProb& q = P->prob[pi];
+    const int4 e = list[it];
+    pi = e.x >> 24;
+    const int t = e.x & 0xFFFFFF;
+    const GProb& q = probs[pi];
     nt = t / q.m_tiles;
     mt = t - nt * q.m_tiles;
-    kb0 = rank * q.G / P->C;
-    kb1 = (rank + 1) * q.G / P->C;
+    kb0 = e.y >> 16;
+    kb1 = e.y & 0xFFFF;
     nst = (kb1 - kb0 + S - 1) / S;
   }
   __device__ bool valid() const { return it < ntiles; }
@@ -158,55 +182,79 @@ struct GCur {
   }
 };
 
-// K1 on one token row by a 128-thread warpgroup: exact quantize.cpp:93-145
-// arithmetic (float absmax, s = double(amax) / 127, codes via quant_one), i.e.
-// bit-identical to quantize_rows_* in quant.cu.
-template <typename T>
-__device__ __forceinline__ void quant_row(const T* __restrict__ xr, int K, int8_t* __restrict__ cr,
-                                          double* s_out, float* red, uint32_t tid,
-                                          unsigned* bad) {
-  constexpr int U = 4;
-  const int nv = K >> 2;  // float4 / 4-element groups (K % 128 == 0)
+// Per-CTA copies of the problem table and of the CTA's piece list (kernel
+// parameters and the schedule otherwise cost a dependent L2/HBM round trip on
+// every first touch, microseconds while the weight stream saturates HBM).
+constexpr int kSchedSmem = 256;  // pieces per CTA held in shared memory
+static_assert((kMaxGroup * sizeof(GProb)) % 16 == 0, "schedule copy alignment");
+constexpr int kTableBytes = kMaxGroup * static_cast<int>(sizeof(GProb)) + kSchedSmem * 16 + 64;
+
+// K1 on one token row by the whole CTA (kThreads threads): exact
+// quantize.cpp:93-145 arithmetic (float absmax, s = double(amax) / 127, codes via
+// quant_one), i.e. bit-identical to quantize_rows_* in quant.cu. Every load of a
+// row of up to kThreads * 4 * V elements is issued before the first use (one
+// memory round trip: the row is read while the weight stream saturates HBM, so
+// each dependent round trip costs microseconds), and the codes are computed
+// from the same registers.
+template <int NT, typename T>
+__device__ __forceinline__ void quant_row_cta(const T* __restrict__ xr, int K,
+                                              int8_t* __restrict__ cr, double* s_out, float* red,
+                                              uint32_t tid, unsigned* bad) {
+  constexpr int V = 8;
+  constexpr int kBatch = NT * V;  // 4-element groups per batch
+  const int nv = K >> 2;          // K % 128 == 0
+  float v[V][4];
   float mx = 0.0f;
   bool fin = true;
-  for (int v0 = static_cast<int>(tid); v0 < nv; v0 += 128 * U) {
-    float v[U][4];
+  for (int b0 = 0; b0 < nv; b0 += kBatch) {
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (v0 + u * 128 < nv) load4<T>(xr + 4 * (v0 + u * 128), v[u]);
+    for (int u = 0; u < V; ++u) {
+      const int e = b0 + u * NT + static_cast<int>(tid);
+      if (e < nv) load4<T>(xr + 4 * e, v[u]);
+    }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (v0 + u * 128 < nv)
+    for (int u = 0; u < V; ++u) {
+      const int e = b0 + u * NT + static_cast<int>(tid);
+      if (e < nv)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          fin = fin && isfinite(v[u][e]);
-          mx = fmaxf(mx, fabsf(v[u][e]));
+        for (int c = 0; c < 4; ++c) {
+          fin = fin && isfinite(v[u][c]);
+          mx = fmaxf(mx, fabsf(v[u][c]));
         }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((tid & 31) == 0) red[tid / 32] = mx;
   if (!fin) atomicOr(bad, 1u);
-  named_bar_sync(4, 128);
-  mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  __syncthreads();
+  mx = 0.0f;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) mx = fmaxf(mx, red[w]);
   const double s = mx == 0.0f ? 1.0 : static_cast<double>(mx) / 127.0;  // quantize.cpp:120-125
   const double r = 1.0 / s;
   if (tid == 0) *s_out = s;
-  for (int v0 = static_cast<int>(tid); v0 < nv; v0 += 128 * U) {
-    float v[U][4];
+  const int last = (nv - 1) / kBatch * kBatch;  // the batch still in registers
+  for (int b0 = 0; b0 < nv; b0 += kBatch) {
+    if (b0 != last) {  // rows longer than one batch (K > NT * 4 * V): reload
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (v0 + u * 128 < nv) load4<T>(xr + 4 * (v0 + u * 128), v[u]);
+      for (int u = 0; u < V; ++u) {
+        const int e = b0 + u * NT + static_cast<int>(tid);
+        if (e < nv) load4<T>(xr + 4 * e, v[u]);
+      }
+    }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (v0 + u * 128 < nv) {
+    for (int u = 0; u < V; ++u) {
+      const int e = b0 + u * NT + static_cast<int>(tid);
+      if (e < nv) {
         uint32_t packed = 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          packed |= (static_cast<uint32_t>(quant_one(v[u][e], s, r, -128, 127)) & 0xFFu)
-                    << (8 * e);
-        *reinterpret_cast<uint32_t*>(cr + 4 * (v0 + u * 128)) = packed;
+        for (int c = 0; c < 4; ++c)
+          packed |= (static_cast<uint32_t>(quant_one(v[u][c], s, r, -128, 127)) & 0xFFu)
+                    << (8 * c);
+        *reinterpret_cast<uint32_t*>(cr + 4 * e) = packed;
       }
+    }
   }
 }
 
@@ -236,16 +284,34 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
   uint64_t* d_empty = d_full + Cf::kND;
   uint64_t* sc_empty = d_empty + Cf::kND;
   uint64_t* pb_full = sc_empty + kStages;   // [2] epilogue -> reduction warps (local)
-  uint64_t* red_full = pb_full + 2;         // [2] all ranks' partials published (cluster)
-  uint64_t* red_empty = red_full + 2;       // [2] all ranks done reading ours (cluster)
+  uint64_t* red_empty = pb_full + 2;        // [2] reduction warps done with a partial buffer
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_empty + 2);
-  float* qred = reinterpret_cast<float*>(bars + 64);  // quantize-phase block max [4]
+  float* qred = reinterpret_cast<float*>(bars + 64);  // quantize-phase block max [16]
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int cid = static_cast<int>(blockIdx.x) / p.C;
-  const int rank = static_cast<int>(blockIdx.x) % p.C;
+  if (threadIdx.x == 0 && p.trace) p.trace[4 * 512 + blockIdx.x] = globaltimer_();
+  const int cta = static_cast<int>(blockIdx.x);
+  uint32_t* flag_s = reinterpret_cast<uint32_t*>(bars + 80);  // split finisher flag
+  uint32_t* epoch_s = flag_s + 1;                                // this launch's epoch
+  GProb* probs_s = reinterpret_cast<GProb*>(reinterpret_cast<uint8_t*>(bars) + 1024);
+  int4* sched_s = reinterpret_cast<int4*>(probs_s + kMaxGroup);
+  const int ntiles = cta < p.NC ? p.sched_len[cta] : 0;
+  const int4* list = ntiles <= kSchedSmem ? sched_s : p.sched + cta * p.sched_stride;
+  if (warp == 3) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(p.prob);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(probs_s);
+    for (int i = lane; i < p.nprob * static_cast<int>(sizeof(GProb) / 4); i += 32) dst[i] = src[i];
+    if (ntiles <= kSchedSmem)
+      for (int i = lane; i < ntiles; i += 32) sched_s[i] = p.sched[cta * p.sched_stride + i];
+  }
 
+  // Launch epoch: every CTA of a launch takes its ticket before the launch lets
+  // its dependents start (griddepcontrol.launch_dependents below), and every
+  // launch has gridDim.x CTAs, so ticket / gridDim.x numbers the launches.
+  unsigned long long ticket = 0;
+  if (threadIdx.x == 0 && p.quantize)
+    ticket = atomicAdd(reinterpret_cast<unsigned long long*>(p.sync + kSyncTicket), 1ull);
   if (warp == 0 && lane == 0) {
     if (p.quantize == 0)
       for (int i = 0; i < p.nprob; ++i) prefetch_tensormap(&maps.m[i]);
@@ -264,44 +330,83 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&pb_full[i], 4);
-      mbar_init(&red_full[i], 2 * p.C);
-      mbar_init(&red_empty[i], 2 * p.C);
+      mbar_init(&red_empty[i], 2);
     }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, Cf::kTmemCols);
   tc_fence_before();
-  if (p.C > 1) cluster_sync_all(); else __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) pdl_launch_dependents();
+  if (threadIdx.x == 0) {
+    *epoch_s = static_cast<unsigned>(ticket / gridDim.x);  // ticket performed before the trigger
+    pdl_launch_dependents();
+  }
+  if (threadIdx.x == 0 && p.trace) p.trace[blockIdx.x] = globaltimer_();
+
+  // Producer lane 0: weights and scales do not depend on the preceding grid or on
+  // the quantize phase, so the first kStages steps go out before
+  // griddepcontrol.wait.
+  auto load_static = [&](const GCur<S>& c, int stage) {
+    const GProb& q = probs_s[c.pi];
+    const int kb = c.kb(), nkb = c.nkb();
+    const int32_t* src = PATH == ISB_PATH_INTEGER_SCALE
+                             ? q.kscale : reinterpret_cast<const int32_t*>(q.fscale);
+    mbar_arrive_expect_tx(&full[stage],
+                          nkb * (kBlockBytes + ((p.dbg & 64) ? 0 : Cf::kXBytes) +
+                                 ((p.dbg & 128) ? 0 : kTileN * 4)));
+    bulk_load_evict_first(smem_w + stage * S * kBlockBytes,
+                          q.packed + (static_cast<int64_t>(c.nt) * q.kblocks + kb) * kBlockBytes,
+                          nkb * kBlockBytes, &full[stage]);
+    if (!(p.dbg & 128))
+      bulk_load(smem_sc + stage * Cf::kScBytes,
+                src + (static_cast<int64_t>(c.nt) * q.G + kb) * kTileN, nkb * kTileN * 4,
+                &full[stage]);
+  };
+  if (p.dbg & 32) {  // launch-overhead probe: setup, dependency wait, teardown only
+    pdl_wait();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc(tmem_base, Cf::kTmemCols);
+    return;
+  }
+  int pre = 0;
+  if (threadIdx.x == 0 && !(p.dbg & 16)) {
+    GCur<S> a;
+    a.init(probs_s, list, ntiles);
+    for (; pre < kStages && a.valid(); ++pre, a.next()) load_static(a, pre);
+  }
+  pdl_wait();  // activations / counters / outputs may belong to the preceding grid
+  if (threadIdx.x == 0 && p.trace) p.trace[5 * 512 + blockIdx.x] = globaltimer_();
+  if (p.quantize && static_cast<int>(blockIdx.x) < p.qtasks) {
+    // ---- quantize phase (whole CTA): token rows blockIdx.x, blockIdx.x + gridDim.x, ...
+    for (int t = blockIdx.x; t < p.qtasks; t += gridDim.x) {
+      int pi = 0;
+      while (t >= p.qoff[pi + 1]) ++pi;
+      const GProb& q = probs_s[pi];
+      const int row = t - p.qoff[pi];
+      int8_t* cr = q.xq + static_cast<int64_t>(row) * q.K;
+      if (q.x_dtype == ISB_F32)
+        quant_row_cta<Cf::kThreads>(static_cast<const float*>(q.xf) + static_cast<int64_t>(row) * q.K,
+                                    q.K, cr, q.sa_w + row, qred, threadIdx.x, &p.sync[kSyncBad]);
+      else
+        quant_row_cta<Cf::kThreads>(
+            static_cast<const __nv_bfloat16*>(q.xf) + static_cast<int64_t>(row) * q.K, q.K, cr,
+            q.sa_w + row, qred, threadIdx.x, &p.sync[kSyncBad]);
+      fence_proxy_async_global();  // codes are read by TMA (async proxy) on other SMs
+      __syncthreads();             // whole row written (and qred consumed)
+      if (threadIdx.x == 0) red_release_gpu_add(&p.sync[pi], 1u);
+    }
+    if (threadIdx.x == 0 && p.trace) p.trace[2 * 512 + blockIdx.x] = globaltimer_();
+  }
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
-    if (elect_one()) {
-      auto load_static = [&](const GCur<S>& c, int stage) {
-        const GProb& q = p.prob[c.pi];
-        const int kb = c.kb(), nkb = c.nkb();
-        const int32_t* src = PATH == ISB_PATH_INTEGER_SCALE
-                                 ? q.kscale : reinterpret_cast<const int32_t*>(q.fscale);
-        mbar_arrive_expect_tx(&full[stage], nkb * (kBlockBytes + Cf::kXBytes + kTileN * 4));
-        bulk_load_evict_first(smem_w + stage * S * kBlockBytes,
-                              q.packed + (static_cast<int64_t>(c.nt) * q.kblocks + kb) * kBlockBytes,
-                              nkb * kBlockBytes, &full[stage]);
-        bulk_load(smem_sc + stage * Cf::kScBytes,
-                  src + (static_cast<int64_t>(c.nt) * q.G + kb) * kTileN, nkb * kTileN * 4,
-                  &full[stage]);
-      };
-      // Weights and scales do not depend on the preceding grid or on the
-      // quantize phase: the first kStages steps go out before griddepcontrol.wait.
-      GCur<S> a;
-      a.init(p, cid, rank);
-      int pre = 0;
-      for (; pre < kStages && a.valid(); ++pre, a.next()) load_static(a, pre);
-      pdl_wait();
+    if (lane == 0) {
       uint32_t seen = 0;
       GCur<S> cur;
-      cur.init(p, cid, rank);
+      cur.init(probs_s, list, ntiles);
       for (int j = 0; cur.valid(); ++j, cur.next()) {
         const int stage = j % kStages;
         if (j >= pre) {
@@ -312,13 +417,15 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
         if (p.quantize && !((seen >> cur.pi) & 1u)) {
           // codes of this problem written by the quantize phase (generic proxy,
           // other SMs): acquire the row count, then order the TMA reads after it
-          wait_rows(&p.sync[cur.pi], static_cast<unsigned>(p.prob[cur.pi].M));
+          if (!(p.dbg & 8))
+            wait_rows(&p.sync[cur.pi], *epoch_s, static_cast<unsigned>(probs_s[cur.pi].M));
           fence_proxy_async_global();
           prefetch_tensormap(&maps.m[cur.pi]);
+          if (seen == 0 && p.trace) p.trace[512 + blockIdx.x] = globaltimer_();
           seen |= 1u << cur.pi;
         }
         const int kb = cur.kb(), nkb = cur.nkb();
-        for (int i = 0; i < nkb; ++i)
+        for (int i = 0; i < nkb && !(p.dbg & 64); ++i)
           tma_load_2d(smem_x + (stage * S + i) * kXSlot, &maps.m[cur.pi], &full[stage],
                       (kb + i) * kBlockK, cur.mt * MT);
       }
@@ -330,7 +437,7 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
     const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
     const uint32_t x_base = smem_u32(smem_x);
     GCur<S> cur;
-    cur.init(p, cid, rank);
+    cur.init(probs_s, list, ntiles);
     for (int j = 0; cur.valid(); ++j, cur.next()) {
       const int stage = j % kStages, as = j % Cf::kNA, ds = j % Cf::kND;
       const int nkb = cur.nkb();
@@ -345,8 +452,9 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
           const uint32_t a_tmem = tbase + as * Cf::kACols + i * 32;
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            mma_i8_ts_warp(d_tmem, a_tmem + c * 8, bdesc + static_cast<uint64_t>(c * 2), idesc,
-                           c > 0 ? 1u : 0u);
+            if (!(p.dbg & 4))
+              mma_i8_ts_warp(d_tmem, a_tmem + c * 8, bdesc + static_cast<uint64_t>(c * 2), idesc,
+                             c > 0 ? 1u : 0u);
         }
       }
       mma_commit_warp(&empty[stage]);
@@ -360,12 +468,13 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
     const uint32_t w_base = smem_u32(smem_w) + r * 16;
     GCur<S> cur;
-    cur.init(p, cid, rank);
+    cur.init(probs_s, list, ntiles);
     for (int j = 0; cur.valid(); ++j, cur.next()) {
       if ((j & 1) != xw) continue;
       const int stage = j % kStages, as = j % Cf::kNA;
       const int nkb = cur.nkb();
       mbar_wait(&full[stage], (j / kStages) & 1);
+      if (j == 0 && threadIdx.x == 128 && p.trace) p.trace[7 * 512 + blockIdx.x] = globaltimer_();
       uint4 q[S][4];
 #pragma unroll
       for (int i = 0; i < S; ++i)
@@ -391,7 +500,7 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
               a[c * 8 + 2 * w + 1] = w4[w] & 0xF0F0F0F0u;     // 16*code(k0+4..k0+7)
             }
           }
-          tmem_st_x32(tmem_base + lane_base + as * Cf::kACols + i * 32, a);
+          if (!(p.dbg & 1)) tmem_st_x32(tmem_base + lane_base + as * Cf::kACols + i * 32, a);
         }
       }
       tmem_wait_st();
@@ -401,36 +510,14 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
     }
   } else if (warp >= 12) {
     // ---------------------------------------------------------------- epilogue
-    const uint32_t tid = threadIdx.x - 384;
     const uint32_t r = (warp % 4) * 32 + lane;  // TMEM lane == output channel in tile
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
-    pdl_wait();  // activations / counters / outputs may belong to the preceding grid
-    if (p.quantize) {
-      // ---- quantize phase: token rows blockIdx.x, blockIdx.x + gridDim.x, ...
-      for (int t = blockIdx.x; t < p.qtasks; t += gridDim.x) {
-        int pi = 0;
-        while (t >= p.qoff[pi + 1]) ++pi;
-        const GProb& q = p.prob[pi];
-        const int row = t - p.qoff[pi];
-        int8_t* cr = q.xq + static_cast<int64_t>(row) * q.K;
-        if (q.x_dtype == ISB_F32)
-          quant_row<float>(static_cast<const float*>(q.xf) + static_cast<int64_t>(row) * q.K, q.K,
-                           cr, q.sa_w + row, qred, tid, &p.sync[kSyncBad]);
-        else
-          quant_row<__nv_bfloat16>(
-              static_cast<const __nv_bfloat16*>(q.xf) + static_cast<int64_t>(row) * q.K, q.K, cr,
-              q.sa_w + row, qred, tid, &p.sync[kSyncBad]);
-        fence_proxy_async_global();  // codes are read by TMA (async proxy) on other SMs
-        named_bar_sync(4, 128);      // whole row written (and qred consumed)
-        if (tid == 0) red_release_gpu_add(&p.sync[pi], 1u);
-      }
-    }
     const uint32_t pbuf_local = smem_u32(pbuf);
     GCur<S> cur;
-    cur.init(p, cid, rank);
+    cur.init(probs_s, list, ntiles);
     int j = 0;
     for (int it = 0; cur.valid(); ++it) {
-      const bool late = p.prob[cur.pi].late_shift != 0;
+      const bool late = probs_s[cur.pi].late_shift != 0;
       int32_t iacc[kCols];
       float facc[kCols];
 #pragma unroll
@@ -455,9 +542,14 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
 #pragma unroll
             for (int cc = 0; cc < kCols; cc += kChunk) {
               uint32_t v[16];
-              if constexpr (kChunk == 16) tmem_ld_x16_(taddr + cc, v);
-              else tmem_ld_x8(taddr + cc, *reinterpret_cast<uint32_t(*)[8]>(&v[0]));
-              tmem_wait_ld();
+              if (!(p.dbg & 2)) {
+                if constexpr (kChunk == 16) tmem_ld_x16_(taddr + cc, v);
+                else tmem_ld_x8(taddr + cc, *reinterpret_cast<uint32_t(*)[8]>(&v[0]));
+                tmem_wait_ld();
+              } else {
+#pragma unroll
+                for (int z = 0; z < 16; ++z) v[z] = z;
+              }
 #pragma unroll
               for (int t = 0; t < kChunk; ++t) {
                 const int32_t d = static_cast<int32_t>(v[t]);  // 16 * P_g, exact
@@ -488,7 +580,7 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
       }
       // hand the tile's partial to the reduction warps
       const int buf = it % Cf::kPbufs;
-      mbar_wait_cluster(&red_empty[buf], ((it / Cf::kPbufs) & 1) ^ 1);
+      mbar_wait(&red_empty[buf], ((it / Cf::kPbufs) & 1) ^ 1);
       const uint32_t pb = pbuf_local + buf * (MT * kTileN * 4);
 #pragma unroll
       for (int t = 0; t < kCols; ++t)
@@ -499,25 +591,33 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&pb_full[buf]);
     }
+    // Last TMEM access of the CTA (every MMA committed, every tcgen05.st waited
+    // before its a_full): release TMEM now. tcgen05.dealloc completes only once
+    // the CTA's outstanding global stores drain, so deallocating after the last
+    // tile's output stores would hold the SM for microseconds under load.
+    tc_fence_before();
+    named_bar_sync(5, 128);
+    if (warp == 12) tmem_dealloc(tmem_base, Cf::kTmemCols);
   } else {
     // ---------------------------------------------------------------- reduction warps (2, 3)
-    pdl_wait();
+    // Whole tiles: Eq. 2 / Eq. 1 straight from the partial buffer. Pieces of a
+    // split tile: partial to the piece's global slot; the piece that completes the
+    // tile's count sums the slots in piece order and finalises.
     const uint32_t u = (warp - 2) * 32 + lane;  // rows u and u + 64
     const uint32_t pbuf_local = smem_u32(pbuf);
-    const int ntiles = cid < p.NC ? p.sched_len[cid] : 0;
-    const int* sched = p.sched + cid * p.sched_stride;
+    const int4* sched = list;
     uint32_t seen = 0;
     auto sa_prefetch = [&](int it) {
       if (it < ntiles) {
-        const int e = sched[it];
-        const int pi = e >> 24;
-        const GProb& q = p.prob[pi];
+        const int4 e = sched[it];
+        const int pi = e.x >> 24;
+        const GProb& q = probs_s[pi];
         if (p.quantize && !((seen >> pi) & 1u)) {
-          wait_rows(&p.sync[pi], static_cast<unsigned>(q.M));
+          wait_rows(&p.sync[pi], *epoch_s, static_cast<unsigned>(q.M));
           seen |= 1u << pi;
         }
         if (u < static_cast<uint32_t>(MT)) {
-          const int64_t m = static_cast<int64_t>((e & 0xFFFFFF) % q.m_tiles) * MT + u;
+          const int64_t m = static_cast<int64_t>((e.x & 0xFFFFFF) % q.m_tiles) * MT + u;
           const uint32_t dst = smem_u32(sa_s + (it & 1) * MT + u);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst),
                        "l"(q.sa + (m < q.M ? m : 0)), "r"(m < q.M ? 8 : 0)
@@ -530,103 +630,136 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
     for (int it = 0; it < ntiles; ++it) {
       const int buf = it % Cf::kPbufs;
       const uint32_t ph = (it / Cf::kPbufs) & 1;
-      const int e = sched[it];
-      const GProb& q = p.prob[e >> 24];
-      const int nt = (e & 0xFFFFFF) / q.m_tiles, mt = (e & 0xFFFFFF) % q.m_tiles;
+      const int4 e = sched[it];
+      const GProb& q = probs_s[e.x >> 24];
+      const int nt = (e.x & 0xFFFFFF) / q.m_tiles, mt = (e.x & 0xFFFFFF) % q.m_tiles;
       sa_prefetch(it + 1);
       cp_async_wait<1>();
       named_bar_sync(2, 64);  // sa_s[it & 1] visible to both reduction warps
       const double* sa_t = sa_s + (it & 1) * MT;
       mbar_wait(&pb_full[buf], ph);
-      if (p.C > 1) {
-        if (lane < static_cast<uint32_t>(p.C))
-          mbar_arrive_remote_release(mapa_shared(smem_u32(&red_full[buf]), lane));
-        mbar_wait_cluster(&red_full[buf], ph);
-      }
       const uint32_t pb = pbuf_local + buf * (MT * kTileN * 4);
-      switch (p.C) {
-        case 1: reduce_tile<MT, 1, PATH>(q, pb, sa_t, rank, nt, mt, u); break;
-        case 2: reduce_tile<MT, 2, PATH>(q, pb, sa_t, rank, nt, mt, u); break;
-        case 4: reduce_tile<MT, 4, PATH>(q, pb, sa_t, rank, nt, mt, u); break;
-        default: reduce_tile<MT, 8, PATH>(q, pb, sa_t, rank, nt, mt, u); break;
+      if (p.dbg & 256) {  // measurement: no epilogue stores / piece reduction
+        named_bar_sync(2, 64);
+        if (lane == 0) mbar_arrive(&red_empty[buf]);
+        continue;
       }
-      named_bar_sync(2, 64);  // done with sa_s[it & 1] before it is refilled
-      if (p.C > 1) {
-        if (lane < static_cast<uint32_t>(p.C))
-          mbar_arrive_remote(mapa_shared(smem_u32(&red_empty[buf]), lane));
-      } else if (lane == 0) {
-        mbar_arrive(&red_empty[buf]);
+      if (e.w < 0) {
+        reduce_tile<MT, 1, PATH>(q, pb, sa_t, 0, nt, mt, u);
+        named_bar_sync(2, 64);  // done with sa_s[it & 1] before it is refilled
+        if (lane == 0) mbar_arrive(&red_empty[buf]);
+        continue;
       }
+      const int piece = e.z >> 16, npieces = e.z & 0xFFFF;
+      uint32_t* slots = p.partials + static_cast<int64_t>(p.split_base[e.w]) * (MT * kTileN);
+      uint32_t* mine = slots + static_cast<int64_t>(piece) * (MT * kTileN);
+#pragma unroll 4
+      for (int t = 0; t < MT; ++t) {
+        mine[t * kTileN + u] = ld_shared_u32(pb + (t * kTileN + u) * 4);
+        mine[t * kTileN + u + 64] = ld_shared_u32(pb + (t * kTileN + u + 64) * 4);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&red_empty[buf]);  // the partial left shared memory
+      // Both warps' slot stores are ordered before thread 0's acq_rel add by the
+      // barrier (release cumulativity), as in a serial split-K semaphore.
+      named_bar_sync(2, 64);
+      if (u == 0) {
+        const unsigned prev = atom_add_acq_rel_gpu(&p.sync[kSyncWords + e.w], 1u);
+        const bool fin = prev == static_cast<unsigned>(npieces - 1);
+        if (fin) p.sync[kSyncWords + e.w] = 0u;  // re-armed for the next launch
+        *flag_s = fin ? 1u : 0u;
+      }
+      named_bar_sync(2, 64);
+      if (*flag_s) {
+        // the last piece in: sum the slots in piece order (every slot's loads in
+        // flight together: one L2 round trip per piece), then the epilogue
+        int32_t is[2][MT];
+        float fs[2][MT];
+#pragma unroll
+        for (int t = 0; t < MT; ++t) { is[0][t] = is[1][t] = 0; fs[0][t] = fs[1][t] = 0.0f; }
+        for (int k = 0; k < npieces; ++k) {
+          const uint32_t* sl = slots + static_cast<int64_t>(k) * (MT * kTileN);
+          uint32_t v[2][MT];
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            v[0][t] = __ldcg(sl + t * kTileN + u);
+            v[1][t] = __ldcg(sl + t * kTileN + u + 64);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+              if (PATH == ISB_PATH_INTEGER_SCALE) is[h][t] += static_cast<int32_t>(v[h][t]);
+              else fs[h][t] += __uint_as_float(v[h][t]);
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t n = static_cast<int64_t>(nt) * kTileN + u + h * 64;
+          if (n < q.N) {
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+              const int64_t m = static_cast<int64_t>(mt) * MT + t;
+              if (m < q.M) {
+                if (PATH == ISB_PATH_INTEGER_SCALE && q.out_dtype == ISB_I32)
+                  static_cast<int32_t*>(q.out)[m * q.N + n] = is[h][t];
+                else
+                  store_out(q.out, q.out_dtype, m * q.N + n,
+                            finish<PATH>(is[h][t], fs[h][t], sa_t[t], q.inv_amp));
+              }
+            }
+          }
+        }
+      }
+      named_bar_sync(2, 64);  // done with sa_s[it & 1] and flag_s
     }
-    // Do not retire while peers may still read our partials.
-    for (int it = max(0, ntiles - Cf::kPbufs); it < ntiles; ++it)
-      mbar_wait_cluster(&red_empty[it % Cf::kPbufs], (it / Cf::kPbufs) & 1);
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc(tmem_base, Cf::kTmemCols);
-  if (p.quantize && threadIdx.x == 0) {
-    // every CTA's polls are behind it: the last one to retire re-arms the counters
-    const unsigned prev = atom_add_acq_rel_gpu(&p.sync[kSyncDone], 1u);
-    if (prev == gridDim.x - 1) {
-      for (int i = 0; i < p.nprob; ++i) p.sync[i] = 0u;
-      p.sync[kSyncDone] = 0u;
-    }
-  }
+  if (threadIdx.x == 0 && p.trace) p.trace[3 * 512 + blockIdx.x] = globaltimer_();
+  if (threadIdx.x == 32 && p.trace) p.trace[8 * 512 + blockIdx.x] = globaltimer_();
+  if (threadIdx.x == 0 && p.trace) p.trace[6 * 512 + blockIdx.x] = globaltimer_();
 }
 
 template <int MT, int PATH>
 void prepare_group_kernel() {
   static std::once_flag once;
   std::call_once(once, [] {
-    auto kern = gemm_w4a8_group<MT, PATH>;
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    Cfg<MT, false>::kSmemBytes),
+    cuda_check(cudaFuncSetAttribute(gemm_w4a8_group<MT, PATH>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Cfg<MT, false>::kSmemBytes + kTableBytes),
                "cudaFuncSetAttribute(smem)");
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-               "cudaFuncSetAttribute(cluster)");
   });
 }
 
 template <int MT, int PATH>
-int group_capacity(int C) {
+int group_blocks_per_sm() {
   prepare_group_kernel<MT, PATH>();
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(C * 64);
-  cfg.blockDim = dim3(Cfg<MT, false>::kThreads);
-  cfg.dynamicSmemBytes = Cfg<MT, false>::kSmemBytes;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemm_w4a8_group<MT, PATH>, &cfg) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gemm_w4a8_group<MT, PATH>,
+                                                           Cfg<MT, false>::kThreads,
+                                                           Cfg<MT, false>::kSmemBytes + kTableBytes),
+             "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
   return n;
 }
 
-int group_capacity_cached(int mt, int path, int C) {
+int group_capacity(int mt, int path, int num_sms) {
   static std::mutex mu;
-  static int cache[2][2][9] = {};
+  static int cache[2][2] = {};
   std::lock_guard<std::mutex> lk(mu);
-  int& slot = cache[mt == 16 ? 0 : 1][path == ISB_PATH_INTEGER_SCALE ? 1 : 0][C];
+  int& slot = cache[mt == 16 ? 0 : 1][path == ISB_PATH_INTEGER_SCALE ? 1 : 0];
   if (!slot) {
     int n = 0;
     if (mt == 16)
-      n = path == ISB_PATH_INTEGER_SCALE ? group_capacity<16, ISB_PATH_INTEGER_SCALE>(C)
-                                         : group_capacity<16, ISB_PATH_FLOAT_SCALE>(C);
+      n = path == ISB_PATH_INTEGER_SCALE ? group_blocks_per_sm<16, ISB_PATH_INTEGER_SCALE>()
+                                         : group_blocks_per_sm<16, ISB_PATH_FLOAT_SCALE>();
     else
-      n = path == ISB_PATH_INTEGER_SCALE ? group_capacity<32, ISB_PATH_INTEGER_SCALE>(C)
-                                         : group_capacity<32, ISB_PATH_FLOAT_SCALE>(C);
+      n = path == ISB_PATH_INTEGER_SCALE ? group_blocks_per_sm<32, ISB_PATH_INTEGER_SCALE>()
+                                         : group_blocks_per_sm<32, ISB_PATH_FLOAT_SCALE>();
     slot = n > 0 ? n : -1;
   }
-  return slot;
+  return slot > 0 ? slot * num_sms : 0;
 }
 
 template <int MT, int PATH>
@@ -635,17 +768,13 @@ void launch_group_mt(const GMaps& maps, const GParams& prm, int grid, cudaStream
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(Cfg<MT, false>::kThreads);
-  cfg.dynamicSmemBytes = Cfg<MT, false>::kSmemBytes;
+  cfg.dynamicSmemBytes = Cfg<MT, false>::kSmemBytes + kTableBytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = prm.C;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
   cuda_check(cudaLaunchKernelEx(&cfg, gemm_w4a8_group<MT, PATH>, maps, prm),
              "gemm_w4a8_group launch");
   count_launch();
@@ -657,14 +786,16 @@ void launch_group_mt(const GMaps& maps, const GParams& prm, int grid, cudaStream
 struct GroupPlan {
   GParams prm{};
   GMaps maps{};
-  int mt = 16, path = ISB_PATH_INTEGER_SCALE, grid = 0, dev = 0;
-  double makespan = 0.0;
-  int* sched_dev = nullptr;   // schedule + lengths
+  int mt = 16, path = ISB_PATH_INTEGER_SCALE, grid = 0, dev = 0, nsplit = 0;
+  double makespan = 0.0;      // per-CTA budget in 128-K blocks (+ per-piece overhead)
+  int* sched_dev = nullptr;   // schedule + lengths + split bases
   unsigned* sync_dev = nullptr;
+  uint32_t* partials = nullptr;
   void* owned = nullptr;      // plan-owned codes / scales when the caller passes none
   ~GroupPlan() {
     if (sched_dev) cudaFree(sched_dev);
     if (sync_dev) cudaFree(sync_dev);
+    if (partials) cudaFree(partials);
     if (owned) cudaFree(owned);
   }
 };
@@ -673,6 +804,38 @@ namespace {
 
 int pick_group_mt(int64_t max_m) {
   return max_m <= 16 ? 16 : 32;  // 33..64 (and beyond) as 32-token tiles (gemm_tc.cu pick_mt)
+}
+
+// McNaughton wrap-around over `ncta` equal budgets. Tiles (cost = their 128-K
+// blocks + a per-piece hand-off overhead) are poured in order; a tile crossing a
+// budget boundary continues on the next CTA. Pieces shorter than one step are
+// avoided by moving the boundary. Returns false if the budget is too small.
+struct Piece { int entry, g0, g1, tile_id; };
+bool wrap_schedule(const std::vector<std::pair<int, int>>& tiles, int ncta, int budget,
+                   int overhead, int min_piece, std::vector<std::vector<Piece>>& lists) {
+  lists.assign(ncta, {});
+  int c = 0, room = budget;
+  for (int i = 0; i < static_cast<int>(tiles.size()); ++i) {
+    const int entry = tiles[i].first, g = tiles[i].second;
+    int g0 = 0;
+    while (g0 < g) {
+      const int rem = g - g0;
+      int take = std::min(rem, room - overhead);
+      if (take < rem && take < min_piece) {  // too small a piece: next CTA
+        if (++c == ncta) return false;
+        room = budget;
+        continue;
+      }
+      lists[c].push_back({entry, g0, g0 + take, i});
+      room -= take + overhead;
+      g0 += take;
+      if (room <= overhead && !(i + 1 == static_cast<int>(tiles.size()) && g0 == g)) {
+        if (++c == ncta) return false;
+        room = budget;
+      }
+    }
+  }
+  return true;
 }
 
 }  // namespace
@@ -697,6 +860,7 @@ GroupPlan* group_plan_create(const isb_group_problem* probs, int nprob, int path
     const isb_weight& w = *q.w;
     if (!w.tensor_core_ok() || w.group != kBlockK)
       fail(ISB_PARAM, "grouped GEMM needs group == 128 and K % 128 == 0");
+    if (w.groups >= (1 << 15)) fail(ISB_PARAM, "grouped GEMM: K too large");
     if (path == ISB_PATH_INTEGER_SCALE && !w.has_int_scales)
       fail(ISB_PARAM, "integer-scale path needs an IntegerScaleSet");
     if (path == ISB_PATH_INTEGER_SCALE &&
@@ -706,6 +870,8 @@ GroupPlan* group_plan_create(const isb_group_problem* probs, int nprob, int path
                              "): the tensor-core integer-scale GEMM cannot be exact");
     if (q.m < 0 || q.m > (1 << 20)) fail(ISB_PARAM, "grouped GEMM: bad M");
     if (q.m > 0 && !q.out) fail(ISB_PARAM, "grouped GEMM: null output");
+    max_m = std::max(max_m, q.m);
+    if (q.m == 0) continue;  // no work (an expert without routed tokens)
     const int qz = q.x != nullptr ? 1 : 0;
     if (quantize >= 0 && qz != quantize)
       fail(ISB_PARAM, "grouped GEMM: either every problem passes float activations or none");
@@ -715,25 +881,26 @@ GroupPlan* group_plan_create(const isb_group_problem* probs, int nprob, int path
         fail(ISB_PARAM, "grouped GEMM: activations must be float32 or bf16");
       if (!q.xq) own_bytes += (q.m * w.k + 255) / 256 * 256;
       if (!q.sa) own_bytes += (q.m * 8 + 255) / 256 * 256;
-    } else if (q.m > 0 && (!q.xq || !q.sa)) {
+    } else if (!q.xq || !q.sa) {
       fail(ISB_PARAM, "grouped GEMM: null activation pointer");
     }
-    max_m = std::max(max_m, q.m);
   }
+  if (quantize < 0) quantize = 0;
   auto* pl = new GroupPlan();
   try {
     cuda_check(cudaGetDevice(&pl->dev), "cudaGetDevice");
     pl->path = path;
     pl->mt = pick_group_mt(max_m);
     const int mt = pl->mt;
-    const int S = mt <= 32 ? 4 : 2;
+    const int S = 4;  // Cfg<16/32>::S
     if (own_bytes) cuda_check(cudaMalloc(&pl->owned, own_bytes), "cudaMalloc(group workspace)");
     uint8_t* own = static_cast<uint8_t*>(pl->owned);
     GParams& P = pl->prm;
     P.nprob = nprob;
     P.quantize = quantize;
-    int min_groups = std::numeric_limits<int>::max();
-    std::vector<int64_t> tiles(nprob);
+    P.dbg = g_dbg;
+    P.trace = g_trace;
+    std::vector<std::pair<int, int>> tiles;  // (entry, groups) in problem order
     P.qoff[0] = 0;
     for (int i = 0; i < nprob; ++i) {
       const isb_group_problem& q = probs[i];
@@ -763,84 +930,100 @@ GroupPlan* group_plan_create(const isb_group_problem* probs, int nprob, int path
       g.late_shift = (path == ISB_PATH_INTEGER_SCALE && w.static_bound > 0 &&
                       w.static_bound <= (int64_t{1} << 27) - 1) ? 1 : 0;
       g.x_dtype = q.x_dtype;
-      tiles[i] = static_cast<int64_t>(w.n_tiles) * g.m_tiles;
-      if (q.m > 0) {
-        min_groups = std::min(min_groups, g.G);
-        pl->maps.m[i] = make_x_map(g.xq, q.m, w.k, mt);
-      }
+      const int64_t nt = static_cast<int64_t>(w.n_tiles) * g.m_tiles;
+      if (static_cast<int64_t>(tiles.size()) + nt >= (int64_t{1} << 24))
+        fail(ISB_PARAM, "grouped GEMM: too many tiles");
+      for (int64_t t = 0; t < nt; ++t) tiles.push_back({(i << 24) | static_cast<int>(t), g.G});
+      if (q.m > 0) pl->maps.m[i] = make_x_map(g.xq, q.m, w.k, mt);
       P.qoff[i + 1] = P.qoff[i] + (quantize ? g.M : 0);
     }
     P.qtasks = P.qoff[nprob];
-    const int64_t total_tiles = std::accumulate(tiles.begin(), tiles.end(), int64_t{0});
-    if (total_tiles >= (int64_t{1} << 24)) fail(ISB_PARAM, "grouped GEMM: too many tiles");
-    // Split-K width C and the schedule: longest-processing-time-first over the
-    // co-resident clusters; a tile costs its steps per rank plus ~half a step of
-    // hand-off (+ the cluster exchange), as in plan_gemm (gemm_tc.cu).
-    static const int force_c = [] {
-      const char* e = std::getenv("ISB_GROUP_C");
+    // Budgets in 128-K blocks: every CTA gets total / ncta (+ a hand-off overhead
+    // of half a step per piece); ISB_GROUP_CTAS overrides the CTA count (A/B).
+    static const int force_ctas = [] {
+      const char* e = std::getenv("ISB_GROUP_CTAS");
       return e ? std::atoi(e) : 0;
     }();
-    double best = 1e30;
-    std::vector<std::vector<int>> best_lists;
-    int best_c = 1;
-    for (int C : {1, 2, 4, 8}) {
-      if (total_tiles == 0) break;
-      if (C > min_groups) break;
-      if (force_c && C != force_c) continue;
-      int cap = group_capacity_cached(mt, path, C);
-      if (cap <= 0) continue;
-      cap = std::min(cap, num_sms / C);
-      const int nc = static_cast<int>(std::min<int64_t>(cap, total_tiles));
-      struct T { double cost; int entry; };
-      std::vector<T> all;
-      all.reserve(static_cast<size_t>(total_tiles));
-      for (int i = 0; i < nprob; ++i) {
-        const int g_cta = (P.prob[i].G + C - 1) / C;
-        const double cost = std::ceil(static_cast<double>(g_cta) / S) + 0.5 + (C > 1 ? 0.25 : 0.0);
-        for (int64_t t = 0; t < tiles[i]; ++t) all.push_back({cost, (i << 24) | static_cast<int>(t)});
-      }
-      std::stable_sort(all.begin(), all.end(), [](const T& a, const T& b) { return a.cost > b.cost; });
-      using L = std::pair<double, int>;
-      std::priority_queue<L, std::vector<L>, std::greater<L>> heap;
-      for (int c = 0; c < nc; ++c) heap.push({0.0, c});
-      std::vector<std::vector<int>> lists(nc);
-      for (const T& t : all) {
-        L l = heap.top();
-        heap.pop();
-        lists[l.second].push_back(t.entry);
-        heap.push({l.first + t.cost, l.second});
-      }
-      double mk = 0.0;
-      while (!heap.empty()) { mk = std::max(mk, heap.top().first); heap.pop(); }
-      if (mk < best - 1e-9) {
-        best = mk;
-        best_c = C;
-        best_lists = std::move(lists);
-      }
+    int ncta = group_capacity(mt, path, num_sms);
+    if (ncta <= 0) fail(ISB_CUDA, "grouped GEMM: kernel does not fit the device");
+    if (force_ctas > 0) ncta = std::min(ncta, force_ctas);
+    int64_t total = 0;
+    for (auto& t : tiles) total += t.second;
+    const int overhead = S / 2;
+    std::vector<std::vector<Piece>> lists;
+    if (!tiles.empty()) {
+      ncta = static_cast<int>(std::min<int64_t>(ncta, total / S + 1));  // >= ~one step each
+      int budget = static_cast<int>((total + overhead * static_cast<int64_t>(tiles.size()) +
+                                     ncta - 1) / ncta) + overhead;
+      while (!wrap_schedule(tiles, ncta, budget, overhead, S, lists)) ++budget;
+      pl->makespan = budget / static_cast<double>(S);
+    } else {
+      ncta = 0;
     }
-    if (total_tiles > 0 && best_lists.empty())
-      fail(ISB_CUDA, "grouped GEMM: no cluster configuration fits the device");
-    P.C = best_c;
-    P.NC = static_cast<int>(best_lists.size());
-    pl->makespan = best;
+    // split tiles: ids, partial slots, counters
+    std::vector<int> pieces_of(tiles.size(), 0);
+    for (auto& l : lists)
+      for (auto& pc : l) ++pieces_of[pc.tile_id];
+    std::vector<int> split_id(tiles.size(), -1), split_base;
+    int slots = 0;
+    for (size_t i = 0; i < tiles.size(); ++i)
+      if (pieces_of[i] > 1) {
+        if (pieces_of[i] >= (1 << 15)) fail(ISB_PARAM, "grouped GEMM: tile split too finely");
+        split_id[i] = static_cast<int>(split_base.size());
+        split_base.push_back(slots);
+        slots += pieces_of[i];
+      }
+    pl->nsplit = static_cast<int>(split_base.size());
+    // Pieces of split tiles first in every CTA's list: their global hand-off
+    // (slot stores, counter, the finisher's slot reads) then overlaps the whole
+    // tiles' weight stream instead of trailing the CTA's last step.
+    for (auto& l : lists)
+      std::stable_partition(l.begin(), l.end(),
+                            [&](const Piece& pc) { return pieces_of[pc.tile_id] > 1; });
+    std::vector<int> seen(tiles.size(), 0);
     size_t stride = 1;
-    for (auto& l : best_lists) stride = std::max(stride, l.size());
-    P.sched_stride = static_cast<int>(stride);
-    std::vector<int> host(static_cast<size_t>(P.NC) * stride + P.NC + 1, 0);
-    for (int c = 0; c < P.NC; ++c) {
-      std::copy(best_lists[c].begin(), best_lists[c].end(), host.begin() + c * stride);
-      host[static_cast<size_t>(P.NC) * stride + c] = static_cast<int>(best_lists[c].size());
+    for (auto& l : lists) stride = std::max(stride, l.size());
+    const size_t n_sched = static_cast<size_t>(ncta) * stride;
+    std::vector<int4> sched(n_sched, int4{0, 0, 0, -1});
+    std::vector<int> lens(ncta, 0);
+    for (int c = 0; c < ncta; ++c) {
+      lens[c] = static_cast<int>(lists[c].size());
+      for (size_t k = 0; k < lists[c].size(); ++k) {
+        const Piece& pc = lists[c][k];
+        const int piece = seen[pc.tile_id]++;
+        sched[c * stride + k] = int4{pc.entry, (pc.g0 << 16) | pc.g1,
+                                     (piece << 16) | pieces_of[pc.tile_id], split_id[pc.tile_id]};
+      }
     }
-    cuda_check(cudaMalloc(&pl->sched_dev, host.size() * sizeof(int)), "cudaMalloc(schedule)");
-    cuda_check(cudaMemcpy(pl->sched_dev, host.data(), host.size() * sizeof(int),
-                          cudaMemcpyHostToDevice),
+    // one device buffer: schedule (int4), lengths, split bases
+    const size_t bytes = n_sched * sizeof(int4) + (lens.size() + split_base.size() + 1) * 4;
+    cuda_check(cudaMalloc(&pl->sched_dev, bytes), "cudaMalloc(schedule)");
+    auto* base = reinterpret_cast<uint8_t*>(pl->sched_dev);
+    cuda_check(cudaMemcpy(base, sched.data(), n_sched * sizeof(int4), cudaMemcpyHostToDevice),
                "copy schedule");
-    P.sched = pl->sched_dev;
-    P.sched_len = pl->sched_dev + static_cast<size_t>(P.NC) * stride;
-    cuda_check(cudaMalloc(&pl->sync_dev, kSyncWords * sizeof(unsigned)), "cudaMalloc(sync)");
-    cuda_check(cudaMemset(pl->sync_dev, 0, kSyncWords * sizeof(unsigned)), "cudaMemset(sync)");
+    int* lens_d = reinterpret_cast<int*>(base + n_sched * sizeof(int4));
+    if (!lens.empty())
+      cuda_check(cudaMemcpy(lens_d, lens.data(), lens.size() * 4, cudaMemcpyHostToDevice),
+                 "copy lengths");
+    int* split_d = lens_d + lens.size();
+    if (!split_base.empty())
+      cuda_check(cudaMemcpy(split_d, split_base.data(), split_base.size() * 4,
+                            cudaMemcpyHostToDevice),
+                 "copy split bases");
+    P.NC = ncta;
+    P.sched = reinterpret_cast<const int4*>(base);
+    P.sched_stride = static_cast<int>(stride);
+    P.sched_len = lens_d;
+    P.split_base = split_d;
+    if (slots)
+      cuda_check(cudaMalloc(&pl->partials, static_cast<size_t>(slots) * mt * kTileN * 4),
+                 "cudaMalloc(partials)");
+    P.partials = pl->partials;
+    const size_t sync_words = kSyncWords + split_base.size();
+    cuda_check(cudaMalloc(&pl->sync_dev, sync_words * sizeof(unsigned)), "cudaMalloc(sync)");
+    cuda_check(cudaMemset(pl->sync_dev, 0, sync_words * sizeof(unsigned)), "cudaMemset(sync)");
     P.sync = pl->sync_dev;
-    pl->grid = P.NC * P.C;
+    pl->grid = ncta;
   } catch (...) {
     delete pl;
     throw;
@@ -868,7 +1051,7 @@ void group_plan_run(GroupPlan* pl, cudaStream_t s) {
 
 void group_plan_info(const GroupPlan* pl, isb_group_info_t* info) {
   info->grid = pl->grid;
-  info->cluster = pl->prm.C;
+  info->cluster = 1;
   info->tile_tokens = pl->mt;
   info->quantize = pl->prm.quantize;
   info->makespan_steps = pl->makespan;

@@ -192,8 +192,10 @@ def test_group_float_scale_within_bound():
         assert float((o.double() - ref).abs().max()) <= float(tol)
 
 
-def test_group_forced_split_widths():
-    """Every split-K width the planner may pick gives the same exact result."""
+def test_group_schedules_with_split_tiles():
+    """Different CTA counts pour the tiles into different budgets (tiles split into
+    pieces reduced through global memory in piece order): the integer result never
+    changes; 20 launches each."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -210,14 +212,29 @@ for m in (1, 16, 40):
         g.run()
     torch.cuda.synchronize()
     for x, w, o in zip(xs, ws, g.outs):
-        assert torch.equal(o, single_reference(x, w, "integer-scale", torch.bfloat16)[2]), (m, g.cluster)
-print("ok", g.cluster)
+        assert torch.equal(o, single_reference(x, w, "integer-scale", torch.bfloat16)[2]), (m, g.grid)
+print("ok", g.grid)
 """ % root
-    for c in ("1", "2", "4", "8"):
+    for n in ("148", "131", "37", "5"):
         r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
-                           env=dict(os.environ, ISB_GROUP_C=c), timeout=600)
+                           env=dict(os.environ, ISB_GROUP_CTAS=n), timeout=600)
         assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-1500:] + r.stderr[-3000:]
-        assert r.stdout.split()[-1] == c
+        assert int(r.stdout.split()[-1]) <= int(n)
+
+
+def test_group_single_small_problem_many_pieces():
+    """One N=K=4096 GEMM at M=16 (32 tiles over ~148 CTAs): every tile is split into
+    several pieces; integer output bit-exact, float within the fp32 bound."""
+    w = layer_weights([(4096, 4096)])[0]
+    x = torch.randn((16, 4096), device=DEV)
+    g = isb.GroupedGemm([{"weight": w, "x": x}], out_dtype=torch.float32)
+    for _ in range(10):
+        g.run()
+    assert torch.equal(g.outs[0], single_reference(x, w, "integer-scale", torch.float32)[2])
+    gf = isb.GroupedGemm([{"weight": w, "x": x}], path="float-scale", out_dtype=torch.float32)
+    o = gf.run()[0].double()
+    ref = single_reference(x, w, "float-scale", torch.float32)[2].double()
+    assert float((o - ref).abs().max()) <= 1e-5 * float(ref.abs().max())
 
 
 def test_group_refuses_unsafe_layer_and_flags_nonfinite():
