@@ -107,6 +107,8 @@ struct GParams {
                             // 16 no weight prefetch before the quantize phase,
                             // 32 launch-overhead probe (no work), 64 no activation
                             // TMA, 128 no scale loads, 256 no output / reduction,
+                            // 2048 pieces finalised locally (wrong sums), 4096 no Eq. 2,
+                            // 8192 no output stores
                             
   int64_t* trace;           // optional per-CTA timeline [4][512] (isb_debug_set_trace)
 };
@@ -142,6 +144,16 @@ ISB_DEVICE void fence_proxy_async_global() {
 ISB_DEVICE void wait_rows(const unsigned* ctr, unsigned epoch, unsigned rows) {
   const unsigned base = epoch * rows;
   while (ld_acquire_gpu(ctr) - base < rows) __nanosleep(32);
+}
+
+// Eq. 2 / Eq. 1 with the token scale pre-multiplied by 2^-e on the integer path:
+// float((double(acc) * 2^-e) * s_a) == float(double(acc) * (s_a * 2^-e)) since both
+// power-of-two scalings are exact (gemm.cpp:252).
+template <int PATH>
+__device__ __forceinline__ float finish_eq(int32_t iacc, float facc, double s) {
+  return __double2float_rn(__dmul_rn(PATH == ISB_PATH_INTEGER_SCALE ? static_cast<double>(iacc)
+                                                                    : static_cast<double>(facc),
+                                     s));
 }
 
 // The CTA's walk over its pieces, one step (S 128-K blocks = S groups of one
@@ -597,6 +609,10 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
     // tile's output stores would hold the SM for microseconds under load.
     tc_fence_before();
     named_bar_sync(5, 128);
+    if (threadIdx.x == 384 && p.trace) {
+      p.trace[9 * 512 + blockIdx.x] = globaltimer_();
+      p.trace[13 * 512 + blockIdx.x] = clock64_();
+    }
     if (warp == 12) tmem_dealloc(tmem_base, Cf::kTmemCols);
   } else {
     // ---------------------------------------------------------------- reduction warps (2, 3)
@@ -633,50 +649,60 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
       const int4 e = sched[it];
       const GProb& q = probs_s[e.x >> 24];
       const int nt = (e.x & 0xFFFFFF) / q.m_tiles, mt = (e.x & 0xFFFFFF) % q.m_tiles;
+      if (it == ntiles - 1 && u == 0 && p.trace) p.trace[12 * 512 + blockIdx.x] = globaltimer_();
       sa_prefetch(it + 1);
       cp_async_wait<1>();
       named_bar_sync(2, 64);  // sa_s[it & 1] visible to both reduction warps
       const double* sa_t = sa_s + (it & 1) * MT;
       mbar_wait(&pb_full[buf], ph);
+      if (it == ntiles - 1 && u == 0 && p.trace) p.trace[10 * 512 + blockIdx.x] = globaltimer_();
+      // The CTA's last tile, if whole, is finalised by all warps after their
+      // roles end (below): on the critical path, 4 outputs per thread instead of
+      // 32 per reduction-warp thread.
+      if (it == ntiles - 1 && e.w < 0 && !(p.dbg & 256)) break;
       const uint32_t pb = pbuf_local + buf * (MT * kTileN * 4);
       if (p.dbg & 256) {  // measurement: no epilogue stores / piece reduction
         named_bar_sync(2, 64);
         if (lane == 0) mbar_arrive(&red_empty[buf]);
         continue;
       }
-      if (e.w < 0) {
-        reduce_tile<MT, 1, PATH>(q, pb, sa_t, 0, nt, mt, u);
-        named_bar_sync(2, 64);  // done with sa_s[it & 1] before it is refilled
-        if (lane == 0) mbar_arrive(&red_empty[buf]);
-        continue;
-      }
-      const int piece = e.z >> 16, npieces = e.z & 0xFFFF;
-      uint32_t* slots = p.partials + static_cast<int64_t>(p.split_base[e.w]) * (MT * kTileN);
-      uint32_t* mine = slots + static_cast<int64_t>(piece) * (MT * kTileN);
-#pragma unroll 4
-      for (int t = 0; t < MT; ++t) {
-        mine[t * kTileN + u] = ld_shared_u32(pb + (t * kTileN + u) * 4);
-        mine[t * kTileN + u + 64] = ld_shared_u32(pb + (t * kTileN + u + 64) * 4);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&red_empty[buf]);  // the partial left shared memory
-      // Both warps' slot stores are ordered before thread 0's acq_rel add by the
-      // barrier (release cumulativity), as in a serial split-K semaphore.
-      named_bar_sync(2, 64);
-      if (u == 0) {
-        const unsigned prev = atom_add_acq_rel_gpu(&p.sync[kSyncWords + e.w], 1u);
-        const bool fin = prev == static_cast<unsigned>(npieces - 1);
-        if (fin) p.sync[kSyncWords + e.w] = 0u;  // re-armed for the next launch
-        *flag_s = fin ? 1u : 0u;
-      }
-      named_bar_sync(2, 64);
-      if (*flag_s) {
-        // the last piece in: sum the slots in piece order (every slot's loads in
-        // flight together: one L2 round trip per piece), then the epilogue
-        int32_t is[2][MT];
-        float fs[2][MT];
+      // the tile's accumulators for rows u and u + 64, all MT tokens
+      uint32_t acc[2][MT];
+      if (e.w < 0 || (p.dbg & 2048)) {
 #pragma unroll
-        for (int t = 0; t < MT; ++t) { is[0][t] = is[1][t] = 0; fs[0][t] = fs[1][t] = 0.0f; }
+        for (int t = 0; t < MT; ++t) {
+          acc[0][t] = ld_shared_u32(pb + (t * kTileN + u) * 4);
+          acc[1][t] = ld_shared_u32(pb + (t * kTileN + u + 64) * 4);
+        }
+      } else {
+        // a piece of a split tile: partial to the piece's slot; the piece that
+        // completes the tile's count sums the slots in piece order
+        const int piece = e.z >> 16, npieces = e.z & 0xFFFF;
+        uint32_t* slots = p.partials + static_cast<int64_t>(p.split_base[e.w]) * (MT * kTileN);
+        uint32_t* mine = slots + static_cast<int64_t>(piece) * (MT * kTileN);
+#pragma unroll 4
+        for (int t = 0; t < MT; ++t) {
+          mine[t * kTileN + u] = ld_shared_u32(pb + (t * kTileN + u) * 4);
+          mine[t * kTileN + u + 64] = ld_shared_u32(pb + (t * kTileN + u + 64) * 4);
+        }
+        // Both warps' slot stores are ordered before thread 0's acq_rel add by the
+        // barrier (release cumulativity), as in a serial split-K semaphore.
+        named_bar_sync(2, 64);
+        if (u == 0) {
+          const unsigned prev = atom_add_acq_rel_gpu(&p.sync[kSyncWords + e.w], 1u);
+          const bool fin = prev == static_cast<unsigned>(npieces - 1);
+          if (fin) p.sync[kSyncWords + e.w] = 0u;  // re-armed for the next launch
+          *flag_s = fin ? 1u : 0u;
+        }
+        named_bar_sync(2, 64);
+        if (!*flag_s) {
+          named_bar_sync(2, 64);  // flag_s and sa_s[it & 1] consumed
+          if (lane == 0) mbar_arrive(&red_empty[buf]);
+          continue;
+        }
+        // every slot's loads in flight together: one L2 round trip per piece
+#pragma unroll
+        for (int t = 0; t < MT; ++t) acc[0][t] = acc[1][t] = 0u;
         for (int k = 0; k < npieces; ++k) {
           const uint32_t* sl = slots + static_cast<int64_t>(k) * (MT * kTileN);
           uint32_t v[2][MT];
@@ -689,37 +715,142 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
           for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int t = 0; t < MT; ++t) {
-              if (PATH == ISB_PATH_INTEGER_SCALE) is[h][t] += static_cast<int32_t>(v[h][t]);
-              else fs[h][t] += __uint_as_float(v[h][t]);
+              if (PATH == ISB_PATH_INTEGER_SCALE)
+                acc[h][t] = static_cast<uint32_t>(static_cast<int32_t>(acc[h][t]) +
+                                                  static_cast<int32_t>(v[h][t]));
+              else
+                acc[h][t] = __float_as_uint(__uint_as_float(acc[h][t]) + __uint_as_float(v[h][t]));
             }
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t n = static_cast<int64_t>(nt) * kTileN + u + h * 64;
-          if (n < q.N) {
-#pragma unroll
-            for (int t = 0; t < MT; ++t) {
-              const int64_t m = static_cast<int64_t>(mt) * MT + t;
-              if (m < q.M) {
-                if (PATH == ISB_PATH_INTEGER_SCALE && q.out_dtype == ISB_I32)
-                  static_cast<int32_t*>(q.out)[m * q.N + n] = is[h][t];
-                else
-                  store_out(q.out, q.out_dtype, m * q.N + n,
-                            finish<PATH>(is[h][t], fs[h][t], sa_t[t], q.inv_amp));
-              }
-            }
-          }
         }
       }
-      named_bar_sync(2, 64);  // done with sa_s[it & 1] and flag_s
+      // Eq. 2 / Eq. 1 in place: the outputs overwrite the partial buffer ([t][128]
+      // rows of out_dtype), then leave as 16-byte vector stores along the token
+      // rows — 8x fewer store instructions than one 2-byte store per output, which
+      // stall for microseconds in a memory system saturated by the weight stream
+      // (a bulk-copy store would queue behind the SM's pending weight loads).
+      named_bar_sync(2, 64);  // every source word read before any is overwritten
+      const int ob = q.out_dtype == ISB_F32 || q.out_dtype == ISB_I32 ? 4 : 2;
+      const int64_t n0 = static_cast<int64_t>(nt) * kTileN;
+      const int nvalid = static_cast<int>(min(static_cast<int64_t>(kTileN), q.N - n0));
+      const bool bulk = (q.N * ob) % 16 == 0 && (nvalid * ob) % 16 == 0;
+      // All operands in registers first, then the arithmetic, then the smem
+      // writes: the 32 outputs' conversion chains (I2F.F64, 2 DMUL, F2F, F2F) are
+      // independent and overlap; interleaving them with volatile smem accesses
+      // serialised every chain (~260 cycles per output).
+      double sav[MT];  // integer path: s_a * 2^-e (exact), one DMUL per output left
+#pragma unroll
+      for (int t = 0; t < MT; ++t)
+        sav[t] = PATH == ISB_PATH_INTEGER_SCALE ? sa_t[t] * q.inv_amp : sa_t[t];
+      uint32_t res[2][MT];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          const int32_t is = static_cast<int32_t>(acc[h][t]);
+          const float fs = __uint_as_float(acc[h][t]);
+          if ((PATH == ISB_PATH_INTEGER_SCALE && q.out_dtype == ISB_I32) || (p.dbg & 4096)) {
+            res[h][t] = acc[h][t];
+          } else {
+            const float f = finish_eq<PATH>(is, fs, sav[t]);
+            res[h][t] = ob == 4 ? __float_as_uint(f)
+                        : q.out_dtype == ISB_BF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(f))
+                                                  : __half_as_ushort(__float2half_rn(f));
+          }
+        }
+      if (bulk) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            const uint32_t dst = pb + t * (kTileN * 4) + (u + h * 64) * ob;
+            if (ob == 4)
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(dst), "r"(res[h][t]) : "memory");
+            else
+              asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst),
+                           "h"(static_cast<unsigned short>(res[h][t]))
+                           : "memory");
+          }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            const int64_t m = static_cast<int64_t>(mt) * MT + t;
+            const int64_t n = n0 + u + h * 64;
+            if (n < n0 + nvalid && m < q.M) {
+              if (ob == 4)
+                static_cast<uint32_t*>(q.out)[m * q.N + n] = res[h][t];
+              else
+                static_cast<unsigned short*>(q.out)[m * q.N + n] =
+                    static_cast<unsigned short>(res[h][t]);
+            }
+          }
+      }
+      if (bulk) {
+        // 16-byte vector stores of the staged rows, consecutive threads along a row
+        named_bar_sync(2, 64);
+        const int cpr = nvalid * ob / 16;  // 16-byte chunks per token row
+        int rows = q.M - mt * MT;
+        rows = rows < MT ? rows : MT;
+        for (int c = static_cast<int>(u); c < ((p.dbg & 8192) ? 0 : rows * cpr); c += 64) {
+          const int t = c / cpr, cc = c - t * cpr;
+          const uint4 v = ld_shared_v4(pb + t * (kTileN * 4) + cc * 16);
+          const int64_t m = static_cast<int64_t>(mt) * MT + t;
+          *reinterpret_cast<uint4*>(static_cast<uint8_t*>(q.out) + (m * q.N + n0) * ob + cc * 16) = v;
+        }
+      }
+      if (it == ntiles - 1 && u == 0 && p.trace) p.trace[11 * 512 + blockIdx.x] = globaltimer_();
+      named_bar_sync(2, 64);  // outputs out of the buffer; sa_s[it & 1] and flag_s consumed
+      if (lane == 0) mbar_arrive(&red_empty[buf]);
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0 && p.trace) p.trace[3 * 512 + blockIdx.x] = globaltimer_();
+  if (threadIdx.x == 0 && p.trace) {
+    p.trace[3 * 512 + blockIdx.x] = globaltimer_();
+    p.trace[14 * 512 + blockIdx.x] = clock64_();
+  }
+  if (ntiles > 0 && list[ntiles - 1].w < 0 && !(p.dbg & 256)) {
+    // The last (whole) tile: its partial is in buffer (ntiles-1) % kPbufs (pb_full
+    // and the token scales were waited by the reduction warps before the barrier).
+    const int it = ntiles - 1;
+    const int4 e = list[it];
+    const GProb& q = probs_s[e.x >> 24];
+    const int nt = (e.x & 0xFFFFFF) / q.m_tiles, mt = (e.x & 0xFFFFFF) % q.m_tiles;
+    const uint32_t pb = smem_u32(pbuf) + (it % Cf::kPbufs) * (MT * kTileN * 4);
+    const double* sa_t = sa_s + (it & 1) * MT;
+    const int64_t n0 = static_cast<int64_t>(nt) * kTileN;
+    constexpr int kPer = MT * kTileN / Cf::kThreads;
+    uint32_t v[kPer];
+    double sc[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int idx = static_cast<int>(threadIdx.x) + k * Cf::kThreads;  // t * 128 + r
+      v[k] = ld_shared_u32(pb + idx * 4);
+      sc[k] = sa_t[idx / kTileN];
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int idx = static_cast<int>(threadIdx.x) + k * Cf::kThreads;
+      const int t = idx / kTileN, r = idx % kTileN;
+      const int64_t m = static_cast<int64_t>(mt) * MT + t, n = n0 + r;
+      if (m < q.M && n < q.N) {
+        if (PATH == ISB_PATH_INTEGER_SCALE && q.out_dtype == ISB_I32) {
+          static_cast<int32_t*>(q.out)[m * q.N + n] = static_cast<int32_t>(v[k]);
+        } else {
+          const double s = PATH == ISB_PATH_INTEGER_SCALE ? sc[k] * q.inv_amp : sc[k];
+          store_out(q.out, q.out_dtype, m * q.N + n,
+                    finish_eq<PATH>(static_cast<int32_t>(v[k]), __uint_as_float(v[k]), s));
+        }
+      }
+    }
+  }
   if (threadIdx.x == 32 && p.trace) p.trace[8 * 512 + blockIdx.x] = globaltimer_();
-  if (threadIdx.x == 0 && p.trace) p.trace[6 * 512 + blockIdx.x] = globaltimer_();
+  if (threadIdx.x == 0 && p.trace) {
+    p.trace[6 * 512 + blockIdx.x] = globaltimer_();
+    p.trace[15 * 512 + blockIdx.x] = clock64_();
+  }
 }
 
 template <int MT, int PATH>
@@ -947,6 +1078,14 @@ GroupPlan* group_plan_create(const isb_group_problem* probs, int nprob, int path
     int ncta = group_capacity(mt, path, num_sms);
     if (ncta <= 0) fail(ISB_CUDA, "grouped GEMM: kernel does not fit the device");
     if (force_ctas > 0) ncta = std::min(ncta, force_ctas);
+    // Longest tiles first: a tile about as long as a budget (e.g. LLaMA down_proj,
+    // K = 11008) then lands whole on its own CTA instead of being cut at every
+    // budget boundary, so lists rarely end with a split piece (whose global
+    // hand-off would trail the CTA's last step).
+    std::stable_sort(tiles.begin(), tiles.end(),
+                     [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+                       return a.second > b.second;
+                     });
     int64_t total = 0;
     for (auto& t : tiles) total += t.second;
     const int overhead = S / 2;

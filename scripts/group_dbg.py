@@ -27,7 +27,7 @@ for flags in ([0, 7] if len(sys.argv) < 3 else [int(a) for a in sys.argv[2:]]):
     t = graph_time(lambda i: plans[i % REPLICAS].run())
     print(f"flags={flags}: {t:.2f} us", flush=True)
 lib.isb_debug_set_flags(0)
-tr = torch.zeros((9, 512), dtype=torch.int64, device=dev)
+tr = torch.zeros((17, 512), dtype=torch.int64, device=dev)
 lib.isb_debug_set_trace(tr.data_ptr(), 0)
 plan = isb.GroupedGemm([{"weight": l[3], "x": x} for l, x in zip(layers[0], xs)])
 lib.isb_debug_set_trace(None, 0)
@@ -71,7 +71,7 @@ for name, row in zip(["start", "first X ready", "quantize end", "retire"], rel):
 
 # three consecutive traced grids (replicas 0, 1, 2), absolute timeline
 lib.isb_debug_set_flags(int(os.environ.get("SEQ_FLAGS", "0")))
-trs = [torch.zeros((9, 512), dtype=torch.int64, device=dev) for _ in range(3)]
+trs = [torch.zeros((17, 512), dtype=torch.int64, device=dev) for _ in range(3)]
 tps = []
 for r in range(3):
     lib.isb_debug_set_trace(trs[r].data_ptr(), 0)
@@ -97,5 +97,25 @@ for r in range(3):
     a = (T[r] - z) / 1e3
     md = lambda i: f"{np.median(a[i]):6.2f}"
     print(f"  grid {r}: entry min {a[4].min():6.2f} med {md(4)} | setup done med {md(0)} | "
-          f"pdl released med {md(5)} max {a[5].max():6.2f} | 1st weights med {md(7)} | X ready med {md(1)} | "
-          f"retire med {md(3)} max {a[3].max():6.2f} | dealloc med {md(8)} | exit med {md(6)} max {a[6].max():6.2f}")
+          f"\n           pdl released med {md(5)} max {a[5].max():6.2f} | 1st weights med {md(7)} | X ready med {md(1)} | "
+          f"last handoff med {md(9)} | red: enter last {md(12)} pb_full {md(10)} reduced {md(11)} | exit med {md(6)} max {a[6].max():6.2f}")
+
+a = (T[2] - z) / 1e3
+ex = a[6]
+order = np.argsort(ex)
+print("exit spread: p10 %.2f p50 %.2f p90 %.2f max %.2f" % tuple(np.percentile(ex, [10, 50, 90, 100])))
+print("latest CTAs:", [(int(c), round(float(ex[c] - np.median(ex)), 2), round(float(a[9][c] - np.median(a[9])), 2)) for c in order[-12:]])
+print("earliest CTAs:", [(int(c), round(float(ex[c] - np.median(ex)), 2)) for c in order[:6]])
+qt = int(np.sum([1 for _ in range(0)]))
+print("median exit of CTAs < 64 (quantize rows): %.2f, >= 64: %.2f" % (np.median(ex[:64]), np.median(ex[64:])))
+print("median last-handoff of CTAs < 64: %.2f, >= 64: %.2f" % (np.median(a[9][:64]), np.median(a[9][64:])))
+print("median X-ready of CTAs < 64: %.2f, >= 64: %.2f" % (np.median(a[1][:64]), np.median(a[1][64:])))
+med = np.median(ex)
+for c in list(order[-6:]) + list(order[70:73]):
+    print(f"CTA {int(c):3d}: handoff {a[9][c]-med:6.2f} red_pbfull {a[10][c]-med:6.2f} retire {a[3][c]-med:6.2f} exit {a[6][c]-med:6.2f} | Xready {a[1][c]-med:6.2f} 1stW {a[7][c]-med:6.2f}")
+import ctypes
+print("list lengths / items of late CTAs:")
+
+cl = trs[2].cpu().numpy()[13:16, :tps[0].grid].astype(np.float64)
+for c in list(order[-4:]) + list(order[70:72]):
+    print(f"CTA {int(c):3d} clocks: retire-handoff {cl[1][c]-cl[0][c]:8.0f}  exit-retire {cl[2][c]-cl[1][c]:8.0f}")
