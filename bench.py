@@ -5,9 +5,12 @@
 Workload (BASELINE.json configs[1]): the LLaMA-2-7B linear layers of one decoder
 layer at decode M=16 tokens (q/k/v fused 4096->12288, o 4096->4096, gate/up fused
 4096->22016, down 11008->4096), group 128, alpha 1024. One step = the hot path
-over one layer: K1 per-token int8 quantize of each layer input + K3 integer-scale
-GEMM per linear. Weights are rotated over 3 layer replicas (3 x 107.5 MB > 2 x
-126 MB L2) so each step streams its weights from HBM.
+over one layer: per-token int8 quantize of each linear's float32 input + the
+integer-scale GEMM of every linear, as ONE grouped layer launch
+(csrc/gemm_group.cu; K1 folded in, the 4 linears' tiles spread over all SMs).
+The per-linear form (K1 + K3 per linear, 8 launches) is timed beside it.
+Weights are rotated over 3 layer replicas (3 x 107.5 MB > 2 x 126 MB L2) so each
+step streams its weights from HBM.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -307,6 +310,74 @@ def dense_layer_timing(isb, m, dev, wd, iters=10):
     return res
 
 
+def grouped_plans(isb, layers, xs, path, out_dtype=None):
+    import torch
+    out_dtype = out_dtype or torch.bfloat16
+    return [isb.GroupedGemm([{"weight": l[3], "x": x} for l, x in zip(layers[r], xs)],
+                            path=path, out_dtype=out_dtype) for r in range(REPLICAS)]
+
+
+def graph_of(fns):
+    """One CUDA graph per replica callable (captured on a side stream)."""
+    import torch
+    for f in fns:
+        f()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graphs = []
+    with torch.cuda.stream(s):
+        for f in fns:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                f()
+            graphs.append(g)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    return graphs
+
+
+def replica_stepper(runs, steps, warmup):
+    """Step i runs replica i % R. Steps are replayed from CUDA graphs holding 4R
+    consecutive steps (programmatic dependent launch between them) — as a serving
+    loop replays one graph per decode iteration holding every layer — so the timed
+    region is K launches back to back; steps that do not fill a group replay
+    one-step graphs. Returns fn(i) enqueuing step i."""
+    R = len(runs)
+    singles = graph_of(runs)
+    G = 4  # rounds of the R replicas per group graph
+    group = graph_of([lambda: [f() for _ in range(G) for f in runs]])[0]
+    first_timed = warmup
+    total = warmup + steps
+
+    def fn(i):
+        # full R-step groups inside the timed region start at multiples of R after warmup
+        j = i - first_timed
+        if i >= first_timed and j % (G * R) == 0 and i + G * R <= total:
+            group.replay()
+        elif i >= first_timed and j % (G * R) != 0 and (i - j % (G * R)) + G * R <= total:
+            pass  # covered by the group replay issued at the group's first step
+        else:
+            singles[(i - first_timed) % R].replay()
+    return fn
+
+
+def grouped_layer_us(isb, layers, xs, path, iters=100):
+    """Device time of one grouped layer launch (graph of `iters` launches rotating the
+    weight replicas, CUDA events on the replay stream)."""
+    import torch
+    plans = grouped_plans(isb, layers, xs, path)
+    g = graph_of([lambda: [plans[i % REPLICAS].run() for i in range(iters)]])[0]
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / iters, plans[0]
+
+
 def run_ours(args, ws, rank, local):
     import numpy as np
     import torch
@@ -318,72 +389,83 @@ def run_ours(args, ws, rank, local):
     layers, xs = build_layers(isb, m, dev, seed=1234 + rank)
     max_k = max(l[4] for lin in layers for l in lin)
     ops_per_step = sum(2 * m * k * n for _, k, n in LAYER)
+    # algorithmic bytes of the grouped step: float32 activations read in-kernel (x_b=4)
+    layer_bytes = sum(alg_bytes(m, k, n, x_b=4) for _, k, n in LAYER)
 
-    # ---- headline: graph-captured layer steps (K1 + K3 per linear)
-    step = LayerStep(isb, layers, xs, m, "int", dev)
-    step.capture()
+    # ---- headline: one grouped layer launch per step (K1 folded in), CUDA graph per replica
+    plans = grouped_plans(isb, layers, xs, "integer-scale")
+    step_fn = replica_stepper([p.run for p in plans], args.steps, args.warmup)
     with ClockSampler(local) as clk:
-        ms = time_steps(step.replay, args.steps, args.warmup, ws)
+        ms = time_steps(step_fn, args.steps, args.warmup, ws)
     ms = max_over_ranks(ms, ws)
     ms_per_step = ms / args.steps
+    us_step = ms_per_step * 1e3
     value = ws * ops_per_step / (ms_per_step * 1e-3) / 1e12  # TOPS, whole job
 
-    # ---- float-scale denominator, identical structure
-    fstep = LayerStep(isb, layers, xs, m, "float", dev)
-    fstep.capture()
-    fms = max_over_ranks(time_steps(fstep.replay, args.steps, args.warmup, ws), ws) / args.steps
-    # ---- the same step with K1 fused into the GEMM (one launch per linear, config C3)
-    fzstep = LayerStep(isb, layers, xs, m, "int", dev, fused=True)
-    fzstep.capture()
-    fzms = max_over_ranks(time_steps(fzstep.replay, args.steps, args.warmup, ws), ws) / args.steps
+    # ---- float-scale denominator, identical structure (grouped K4)
+    fplans = grouped_plans(isb, layers, xs, "float-scale")
+    fms = max_over_ranks(time_steps(replica_stepper([p.run for p in fplans], args.steps,
+                                                    args.warmup), args.steps, args.warmup, ws),
+                         ws) / args.steps
+    # ---- per-linear form: K1 + K3 per linear (8 launches), the round-1 step
+    step = LayerStep(isb, layers, xs, m, "int", dev)
+    step.capture()
+    ums = max_over_ranks(time_steps(step.replay, args.steps, args.warmup, ws), ws) / args.steps
 
     # ---- e2e: host pinned X in, host bf16 out, every step, through the public runtime
-    # API (paper_2405_14597_b200.runtime.GraphedLinears: H2D copies, K1 + K3 per
-    # linear and D2H copies recorded once into a CUDA graph, replayed per step).
+    # API (paper_2405_14597_b200.runtime.GraphedLinears, grouped mode: H2D copies, one
+    # grouped layer launch, D2H copies recorded into one CUDA graph, replayed per step).
     from paper_2405_14597_b200.runtime import GraphedLinears
     runners = []
     for r in range(REPLICAS):
-        g = GraphedLinears([l[3] for l in layers[r]], m, device=dev)
+        g = GraphedLinears([l[3] for l in layers[r]], m, device=dev, mode="grouped")
         for j, x in enumerate(xs):
             g.host_inputs[j].copy_(x.cpu())
         runners.append(g.capture())
     e2e_ms = max_over_ranks(time_steps(lambda i: runners[i % REPLICAS].run(), args.steps,
                                        args.warmup, ws), ws) / args.steps
     h2d, d2h = runners[0].h2d_bytes, runners[0].d2h_bytes
+    # alternative runtime mode: one single-problem grouped launch per linear, the PCIe
+    # transfers overlapping the GEMMs
+    prunners = []
+    for r in range(REPLICAS):
+        g = GraphedLinears([l[3] for l in layers[r]], m, device=dev, mode="pipelined")
+        for j, x in enumerate(xs):
+            g.host_inputs[j].copy_(x.cpu())
+        prunners.append(g.capture())
+    e2e_pipe_ms = max_over_ranks(time_steps(lambda i: prunners[i % REPLICAS].run(), args.steps,
+                                            args.warmup, ws), ws) / args.steps
     # the same through per-call eager API calls (host launch overhead included)
     xh = [x.cpu().pin_memory() for x in xs]
     oh = [torch.empty((m, n), dtype=torch.bfloat16).pin_memory() for _, _, n in LAYER]
     xd = [torch.empty_like(x) for x in xs]
-    e2e_ws = [isb.Workspace() for _ in range(REPLICAS)]
+    eplans = [isb.GroupedGemm([{"weight": l[3], "x": x} for l, x in zip(layers[r], xd)])
+              for r in range(REPLICAS)]
 
     def e2e_eager(i):
-        r = i % REPLICAS
-        for j, (_, k, n, w, _) in enumerate(layers[r]):
+        p = eplans[i % REPLICAS]
+        for j in range(len(LAYER)):
             xd[j].copy_(xh[j], non_blocking=True)
-            q, sa = isb.quantize_per_token(xd[j])
-            out = isb.gemm_integer_scale(q, sa, w, workspace=e2e_ws[r])
-            oh[j].copy_(out, non_blocking=True)
+        p.run()
+        for j in range(len(LAYER)):
+            oh[j].copy_(p.outs[j], non_blocking=True)
 
     e2e_eager_ms = max_over_ranks(time_steps(e2e_eager, min(args.steps, 200), args.warmup, ws),
                                   ws) / min(args.steps, 200)
 
-    # ---- dominant kernel roofline (K3), events on the launching stream
+    # ---- per-linear kernel table (single-GEMM kernels, events on the launching stream)
     xq_sa = [isb.quantize_per_token(x) for x in xs]
     kt = gemm_kernel_timing(isb, layers, xq_sa, m, "int")
     kf = gemm_kernel_timing(isb, layers, xq_sa, m, "float")
-    tot_bytes = sum(r["alg_bytes"] for r in kt)
-    tot_us = sum(r["us"] for r in kt)
     peak, peak_kind = load_peaks()
-    # Dominant kernel: K3 on the largest linear (gate_up, 4096 -> 22016) — algorithmic
-    # bytes of one launch / its average launch duration.
-    dom = max(kt, key=lambda r: r["alg_bytes"])
-    achieved = dom["alg_bytes"] / dom["us"] / 1e3  # GB/s
+    # Dominant kernel: the grouped layer launch (the whole step is this one kernel).
+    achieved = layer_bytes / us_step / 1e3  # GB/s
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "k3_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(tpath) and m == 16:
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get("bytes_per_launch_gate_up_m16")
+                traffic = json.load(f).get("grouped_layer_m16_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -392,34 +474,46 @@ def run_ours(args, ws, rank, local):
           for _ in range(REPLICAS)]
     dense_m = dense_layer_timing(isb, m, dev, wd, iters=30)
 
-    # ---- prefill / decode sweep of the whole layer (kernel-only, int vs float vs fp16)
-    sweep = []
+    # ---- decode / prefill sweep of the whole layer: int vs float vs fp16 dense
+    sweep, tensor_roof = [], None
     if not args.no_sweep:
         for mm in args.sweep:
-            lay = layers
-            xq = [isb.quantize_per_token(torch.randn((mm, k), device=dev)) for _, k, _ in LAYER]
-            ti = gemm_kernel_timing(isb, lay, xq, mm, "int", iters=10)
-            tf = gemm_kernel_timing(isb, lay, xq, mm, "float", iters=10)
-            us_i = sum(r["us"] for r in ti)
-            us_f = sum(r["us"] for r in tf)
-            us_d = sum(dense_layer_timing(isb, mm, dev, wd, iters=10 if mm <= 256 else 4))
             ops = sum(2 * mm * k * n for _, k, n in LAYER)
-            byts = sum(r["alg_bytes"] for r in ti)
-            sweep.append({"M": mm, "us_per_layer_int": round(us_i, 2),
-                          "us_per_layer_float": round(us_f, 2),
-                          "speedup_vs_float": round(us_f / us_i, 3),
-                          "us_per_layer_fp16_dense": round(us_d, 2),
-                          "speedup_vs_fp16_dense": round(us_d / us_i, 3),
-                          "tops_int": round(ops / us_i / 1e6, 1),
-                          "hbm_frac_int": round(byts / us_i / 1e3 / peak, 3),
-                          # int8 tensor roofline: nominal 4.5 POPS; measured 4.79 POPS
-                          # (tcgen05 kind::i8 128x256, profiles/r01_mma_peak.txt)
-                          "tensor_frac_int_nominal": round(ops / us_i / 1e6 / 4500.0, 3),
-                          "tensor_frac_int_measured": round(ops / us_i / 1e6 / 4786.0, 3)})
+            us_d = sum(dense_layer_timing(isb, mm, dev, wd, iters=10 if mm <= 256 else 4))
+            row = {"M": mm}
+            if mm <= 64:
+                xm = [torch.randn((mm, k), device=dev) for _, k, _ in LAYER]
+                us_i, pl = grouped_layer_us(isb, layers, xm, "integer-scale")
+                us_f, _ = grouped_layer_us(isb, layers, xm, "float-scale")
+                byts = sum(alg_bytes(mm, k, n, x_b=4) for _, k, n in LAYER)
+                row["kernel"] = f"grouped layer launch (K1 fused), MT={pl.tile_tokens}"
+            else:
+                xq = [isb.quantize_per_token(torch.randn((mm, k), device=dev)) for _, k, _ in LAYER]
+                ti = gemm_kernel_timing(isb, layers, xq, mm, "int", iters=10)
+                tf = gemm_kernel_timing(isb, layers, xq, mm, "float", iters=10)
+                us_i = sum(r["us"] for r in ti)
+                us_f = sum(r["us"] for r in tf)
+                byts = sum(r["alg_bytes"] for r in ti)
+                row["kernel"] = "per-linear prefill kernels (int: k_g-folded SS-256, float: MT=128)"
+                row["per_linear_int"] = ti
+            row.update({"us_per_layer_int": round(us_i, 2), "us_per_layer_float": round(us_f, 2),
+                        "speedup_vs_float": round(us_f / us_i, 3),
+                        "us_per_layer_fp16_dense": round(us_d, 2),
+                        "speedup_vs_fp16_dense": round(us_d / us_i, 3),
+                        "tops_int": round(ops / us_i / 1e6, 1),
+                        "hbm_frac_int": round(byts / us_i / 1e3 / peak, 3),
+                        # int8 tensor roofline: nominal 4.5 POPS; measured 4.79 POPS
+                        # (tcgen05 kind::i8 128x256, profiles/r01_mma_peak.txt)
+                        "tensor_frac_int_nominal": round(ops / us_i / 1e6 / 4500.0, 3),
+                        "tensor_frac_int_measured": round(ops / us_i / 1e6 / 4786.0, 3)})
+            sweep.append(row)
+            if mm == 2048:
+                tensor_roof = {"bound": "tensor", "achieved": round(ops / us_i / 1e6, 1),
+                               "peak": 4786.0, "peak_kind": "measured tcgen05 kind::i8 (r01_mma_peak)",
+                               "unit": "TOPS", "frac": round(ops / us_i / 1e6 / 4786.0, 4),
+                               "frac_nominal_4500": round(ops / us_i / 1e6 / 4500.0, 4),
+                               "kernel": "gemm_w4a8_fold_ss<256> per linear, M=2048 layer"}
 
-    # ---- Mixtral-8x7B expert FFN (config C5): 8 experts on this GPU, T=16 decode
-    # tokens top-2 routed (32 expert rows, 4 per expert), per expert K1 + gate/up
-    # GEMM (4096 -> 2 x 14336) + SiLU*up + K1 + down GEMM (14336 -> 4096); graph.
     moe_res = None
     if not args.no_moe:
         moe_res = moe_bench(isb, dev, args)
@@ -432,7 +526,7 @@ def run_ours(args, ws, rank, local):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 5),
-        "us_per_layer": round(ms_per_step * 1e3, 2),
+        "us_per_layer": round(us_step, 2),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -442,33 +536,38 @@ def run_ours(args, ws, rank, local):
             "workload": f"llama2-7b decoder-layer linears, decode M={m}",
             "M": m, "linears": [{"name": a, "K": k, "N": n} for a, k, n in LAYER],
             "group": GROUP, "alpha": ALPHA, "max_int_scale": max_k,
-            "step": "K1 per-token quantize + K3 integer-scale GEMM per linear (8 kernels, CUDA graph)",
+            "step": "one grouped layer launch: per-token quantize of the 4 float32 inputs + "
+                    "integer-scale GEMM of the 4 linears (gemm_w4a8_group, CUDA graph)",
             "l2": f"weights rotated over {REPLICAS} layer replicas ({REPLICAS}x107.5MB > 2x126MB L2)",
             "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
         },
-        "speedup_vs_float_scale": round(fms / ms_per_step, 3),
+        "speedup_vs_float_scale": round(fms * 1e3 / us_step, 3),
         "float_scale_us_per_layer": round(fms * 1e3, 2),
-        "act_fused_us_per_layer": round(fzms * 1e3, 2),
+        "per_linear_us_per_layer": round(ums * 1e3, 2),
+        "per_linear_step": "K1 + K3 per linear (8 launches, CUDA graph)",
+        "grouped_plan": {"grid": plans[0].grid, "tile_tokens": plans[0].tile_tokens,
+                         "budget_steps_per_cta": plans[0].makespan_steps},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic,
-                     "kernel": f"gemm_w4a8_tc<integer-scale> {dom['linear']} M={m} K={dom['K']} N={dom['N']}",
-                     "alg_bytes_per_launch": dom["alg_bytes"], "us_per_launch": dom["us"],
-                     "layer_alg_bytes": tot_bytes, "layer_kernel_us": round(tot_us, 2),
-                     "layer_frac": round(tot_bytes / tot_us / 1e3 / peak, 4),
-                     "per_linear": kt},
+                     "kernel": f"gemm_w4a8_group<{plans[0].tile_tokens}, integer-scale> "
+                               f"LLaMA-2-7B layer M={m} (4 linears, K1 fused)",
+                     "alg_bytes_per_launch": layer_bytes, "us_per_launch": round(us_step, 3),
+                     "per_linear_single_gemm": kt},
+        "roofline_tensor_prefill": tensor_roof,
         "float_scale_kernel": kf,
         "fp16_dense": {"kernel": "gemm_f16_tc (tcgen05 kind::f16, fp32 acc, no cuBLAS)",
                        "us_per_linear": [round(v, 2) for v in dense_m],
                        "us_per_layer": round(sum(dense_m), 2),
-                       "speedup_w4a8_kernels_vs_fp16": round(sum(dense_m) / tot_us, 3),
-                       "speedup_w4a8_step_vs_fp16": round(sum(dense_m) / (ms_per_step * 1e3), 3)},
+                       "speedup_w4a8_step_vs_fp16": round(sum(dense_m) / us_step, 3)},
         "e2e": {"value": round(ws * ops_per_step / (e2e_ms * 1e-3) / 1e12, 3), "unit": "TOPS",
                 "us_per_layer": round(e2e_ms * 1e3, 2),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "runtime.GraphedLinears (H2D + K1/K3 x4 + D2H in one CUDA graph)",
+                "api": "runtime.GraphedLinears (mode=grouped): H2D of the 4 float32 inputs -> "
+                       "one grouped launch (K1 fused) -> D2H of the 4 bf16 outputs, one CUDA graph",
+                "pipelined_mode_us_per_layer": round(e2e_pipe_ms * 1e3, 2),
                 "eager_api_us_per_layer": round(e2e_eager_ms * 1e3, 2)},
-        "gpu_launches": args.steps * step.kernels_per_step,
+        "gpu_launches": args.steps * 1,
         "clocks": clk.summary(),
         "sweep": sweep,
         "mixtral_moe": moe_res,
@@ -477,6 +576,10 @@ def run_ours(args, ws, rank, local):
 
 
 def moe_bench(isb, dev, args, n_experts=8, tokens=16, k=4096, f=14336):
+    """Config C5 on one GPU: Mixtral-8x7B expert FFN, T=16 decode tokens top-2 routed
+    (32 expert rows, 4 per expert). Per step: ONE grouped launch for the 8 experts'
+    w1|w3 GEMMs (4096 -> 2 x 14336, K1 fused), SiLU(gate) * up (torch elementwise),
+    ONE grouped launch for the 8 experts' w2 GEMMs (14336 -> 4096, K1 fused); CUDA graph."""
     import torch
     gen = torch.Generator(device=dev)
     gen.manual_seed(77)
@@ -490,36 +593,30 @@ def moe_bench(isb, dev, args, n_experts=8, tokens=16, k=4096, f=14336):
             del wf
             si = isb.integerize_scales(scales.cpu().numpy(), ALPHA)
             packs.append(isb.PackedWeight.from_codes(codes, GROUP, scales, si.int_scales, ALPHA))
-            byts += alg_bytes(rows, kk, nn)
+            byts += alg_bytes(rows, kk, nn, x_b=4)
         experts.append(packs)
-    x = [torch.randn((rows, k), generator=gen, device=dev) for _ in range(n_experts)]
-    gu = [torch.empty((rows, 2 * f), dtype=torch.float32, device=dev) for _ in range(n_experts)]
-    y = [torch.empty((rows, k), dtype=torch.bfloat16, device=dev) for _ in range(n_experts)]
-    wsp = isb.Workspace()
+    x = torch.randn((n_experts, rows, k), generator=gen, device=dev)
+    gu = torch.empty((n_experts, rows, 2 * f), dtype=torch.float32, device=dev)
+    h = torch.empty((n_experts, rows, f), dtype=torch.float32, device=dev)
+    y = torch.empty((n_experts, rows, k), dtype=torch.bfloat16, device=dev)
+    g13 = isb.GroupedGemm([{"weight": experts[e][0], "x": x[e], "out": gu[e]}
+                           for e in range(n_experts)], out_dtype=torch.float32)
+    g2 = isb.GroupedGemm([{"weight": experts[e][1], "x": h[e], "out": y[e]}
+                          for e in range(n_experts)], out_dtype=torch.bfloat16)
 
-    def step(_i):
-        for e, (w13, w2) in enumerate(experts):
-            q, sa = isb.quantize_per_token(x[e])
-            isb.gemm_integer_scale(q, sa, w13, out=gu[e], workspace=wsp)
-            h = torch.nn.functional.silu(gu[e][:, :f]) * gu[e][:, f:]
-            hq, hs = isb.quantize_per_token(h)
-            isb.gemm_integer_scale(hq, hs, w2, out=y[e], workspace=wsp)
+    def step():
+        g13.run()
+        torch.mul(torch.nn.functional.silu(gu[..., :f]), gu[..., f:], out=h)
+        g2.run()
 
-    step(0)
-    torch.cuda.synchronize()
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(s):
-        with torch.cuda.graph(g, stream=s):
-            step(0)
-    torch.cuda.current_stream().wait_stream(s)
+    g = graph_of([step])[0]
     n = max(20, min(args.steps, 200))
     ms = time_steps(lambda i: g.replay(), n, args.warmup, 1) / n
     ops_ = n_experts * 2 * rows * (k * 2 * f + f * k)
     peak, _ = load_peaks()
     return {"config": f"Mixtral-8x7B expert FFN, {n_experts} experts on 1 GPU, {tokens} tokens "
-                      f"top-2 ({rows} rows/expert), K1+GEMM+SiLU+K1+GEMM per expert, CUDA graph",
+                      f"top-2 ({rows} rows/expert): grouped w1|w3 launch (K1 fused) + SiLU*up "
+                      f"(torch) + grouped w2 launch (K1 fused), CUDA graph",
             "us_per_moe_layer": round(ms * 1e3, 2), "tops": round(ops_ / (ms * 1e-3) / 1e12, 2),
             "alg_bytes": byts, "hbm_frac": round(byts / (ms * 1e-3) / 1e9 / peak, 3)}
 
@@ -612,8 +709,13 @@ def run_reference(args, ws, rank):
 
 
 def cpu_baseline(args):
-    threads = min(os.cpu_count() or 1, args.m)
+    """The oracle port of gemm_integer_scale on this box's host cores, one LLaMA-2-7B
+    layer's 4 linears at M rows, median of 3 like run_bench (analysis.cpp:195-215),
+    at workers = nproc (the reported value) and workers = 1."""
+    nproc = os.cpu_count() or 1
+    threads = min(nproc, args.m)  # the reference parallelises over rows only (gemm.cpp:63-68)
     tops, sec, _ = cpu_layer_sample(args.m, threads, repeats=3)
+    tops1, sec1, _ = cpu_layer_sample(args.m, 1, repeats=3)
     try:
         model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo")
                      if l.startswith("model name"))
@@ -622,8 +724,11 @@ def cpu_baseline(args):
     return {"value": tops, "unit": "TOPS", "cores": threads, "kind": "port",
             "sample": (f"one LLaMA-2-7B layer's 4 linears at M={args.m}, median of 3 "
                        f"({sec * 1e3:.0f} ms/layer); oracle port of gemm_integer_scale, "
-                       f"{threads} row-partitioned threads of {os.cpu_count()} on {model}; "
-                       f"-O3 -DNDEBUG -ffp-contract=off")}
+                       f"{threads} row-partitioned threads of {nproc} on {model}; "
+                       f"-O3 -DNDEBUG -ffp-contract=off"),
+            "workers_1": {"value": tops1, "ms_per_layer": round(sec1 * 1e3, 1), "cores": 1},
+            "workers_nproc": {"value": tops, "ms_per_layer": round(sec * 1e3, 1),
+                              "cores": threads, "nproc": nproc, "cpu": model}}
 
 
 def main():
@@ -633,12 +738,22 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--m", type=int, default=16)
-    ap.add_argument("--sweep", type=int, nargs="*", default=[1, 16, 64, 2048])
+    ap.add_argument("--sweep", type=int, nargs="*", default=[1, 2, 4, 8, 16, 32, 64, 2048])
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-moe", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched directly with --gpus N: re-exec as N ranks (one process per GPU)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
 
     if args.impl == "reference":
         ws = int(os.environ.get("WORLD_SIZE", "1"))
