@@ -166,6 +166,7 @@ def build_layers(isb, m, dev, seed):
             del wf
             s = isb.integerize_scales(scales.cpu().numpy(), ALPHA)      # offline, host
             w = isb.PackedWeight.from_codes(codes, GROUP, scales, s.int_scales, ALPHA)
+            w.group_scales = scales  # kept for re-integerizing at another amplifier
             del codes
             lin.append((name, k, n, w, int(s.int_scales.max())))
         layers.append(lin)
@@ -308,6 +309,29 @@ def dense_layer_timing(isb, m, dev, wd, iters=10):
         torch.cuda.synchronize()
         res.append(e0.elapsed_time(e1) * 1000.0 / iters)
     return res
+
+
+_A8192 = {}
+
+
+def alpha8192_layers(isb, layers, dev):
+    """The bench layers re-integerized at alpha = 8192 (the paper's LLaMA-3 recipe):
+    same codes and float scales, k_g = round(s * 8192)."""
+    if "l" not in _A8192:
+        out = []
+        for lin in layers[:1]:
+            row = []
+            for name, k, n, w, _ in lin:
+                codes = w.unpack_codes()
+                scales = w.group_scales
+                si = isb.integerize_scales(scales.cpu().numpy(), 8192)
+                row.append((name, k, n, isb.PackedWeight.from_codes(codes, GROUP, scales,
+                                                                   si.int_scales, 8192),
+                            int(si.int_scales.max())))
+            out.append(row)
+        # prefill is tensor-bound: one replica, referenced REPLICAS times
+        _A8192["l"] = out * REPLICAS
+    return _A8192["l"]
 
 
 def grouped_plans(isb, layers, xs, path, out_dtype=None):
@@ -506,6 +530,16 @@ def run_ours(args, ws, rank, local):
                         # (tcgen05 kind::i8 128x256, profiles/r01_mma_peak.txt)
                         "tensor_frac_int_nominal": round(ops / us_i / 1e6 / 4500.0, 3),
                         "tensor_frac_int_measured": round(ops / us_i / 1e6 / 4786.0, 3)})
+            if mm >= 256:
+                # the general integer path (alpha = 8192: k_g up to ~124, no fold) on the
+                # per-group skeleton K4 runs on — integer vs float scale with identical tiling
+                lay8 = alpha8192_layers(isb, layers, dev)
+                t8 = gemm_kernel_timing(isb, lay8, xq, mm, "int", iters=10)
+                us_8 = sum(r["us"] for r in t8)
+                row.update({"us_per_layer_int_alpha8192": round(us_8, 2),
+                            "alpha8192_max_int_scale": max(l[4] for l in lay8[0]),
+                            "speedup_int_alpha8192_vs_float_same_tiling": round(us_f / us_8, 3),
+                            "tops_int_alpha8192": round(ops / us_8 / 1e6, 1)})
             sweep.append(row)
             if mm == 2048:
                 tensor_roof = {"bound": "tensor", "achieved": round(ops / us_i / 1e6, 1),

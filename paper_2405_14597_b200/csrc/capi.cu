@@ -176,6 +176,16 @@ bool fold_disabled() {
   return off;
 }
 
+// ISB_NO_PG=1 keeps prefill-M calls that cannot fold (k_g > 16, float scale) on the
+// decode-family MT=128 kernel (A/B measurements).
+bool pg_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("ISB_NO_PG");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
 // The stream-K decode kernel (gemm_decode.cu) is opt-in: ISB_DECODE=1. At the
 // LLaMA-2-7B decode shapes the cluster split-K kernel (gemm_tc.cu) is faster
 // (profiles/r01_decode_streamk.md); the stream-K kernel is kept for A/B work.
@@ -252,6 +262,10 @@ void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
     fail(ISB_PARAM, "workspace too small: need " + std::to_string(pl.workspace_bytes) + " bytes");
   if (fold_eligible(m, *w, path) && !fold_disabled()) {
     launch_gemm_fold(xq, sa, m, *w, out, out_dtype, num_sms(), as_stream(stream));
+    return;
+  }
+  if (pg_eligible(m, *w) && !pg_disabled()) {  // prefill M: any k_g, and K4
+    launch_gemm_pg(path, xq, sa, m, *w, out, out_dtype, num_sms(), as_stream(stream));
     return;
   }
   launch_gemm_tc(path, xq, sa, m, *w, out, out_dtype, ws, pl, as_stream(stream));

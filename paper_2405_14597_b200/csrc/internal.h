@@ -89,6 +89,11 @@ constexpr int64_t kFoldMinM = 256;
 bool fold_eligible(int64_t m, const isb_weight& w, int path);
 void launch_gemm_fold(const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                       void* out, int out_dtype, int num_sms, cudaStream_t s);
+// Prefill per-group-epilogue K3 (any k_g) / K4 on the SS skeleton (gemm_pg.cu).
+constexpr int64_t kPgMinM = 128;
+bool pg_eligible(int64_t m, const isb_weight& w);
+void launch_gemm_pg(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
+                    void* out, int out_dtype, int num_sms, cudaStream_t s);
 // Decode K3d/K4d (gemm_decode.cu): stream-K over all SMs, two CTAs per SM.
 constexpr int64_t kDecodeMaxM = 32;
 bool decode_eligible(int64_t m, const isb_weight& w);
