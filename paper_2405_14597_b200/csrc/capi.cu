@@ -261,7 +261,12 @@ void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
   if (!ws || ws_bytes < pl.workspace_bytes)
     fail(ISB_PARAM, "workspace too small: need " + std::to_string(pl.workspace_bytes) + " bytes");
   if (fold_eligible(m, *w, path) && !fold_disabled()) {
-    launch_gemm_fold(xq, sa, m, *w, out, out_dtype, num_sms(), as_stream(stream));
+    // 1-CTA SS kernel (gemm_fold.cu) by default; debug flag kDbgPair selects the CTA-pair
+    // experiment (gemm_pair.cu) for A/B measurements in one process.
+    if (g_dbg & kDbgPair)
+      launch_gemm_pair(xq, sa, m, *w, out, out_dtype, num_sms(), as_stream(stream));
+    else
+      launch_gemm_fold(xq, sa, m, *w, out, out_dtype, num_sms(), as_stream(stream));
     return;
   }
   if (pg_eligible(m, *w) && !pg_disabled()) {  // prefill M: any k_g, and K4

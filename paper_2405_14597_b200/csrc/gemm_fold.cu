@@ -560,16 +560,56 @@ __global__ void __launch_bounds__(FoldSS<MT, NA, SX, SW, EW>::kThreads, 1)
             x ^= __bfloat16_as_ushort(__float2bfloat16_rn(__double2float_rn(o)));
           }
           if (x == 0x12345u) static_cast<uint32_t*>(p.out)[0] = x;
-        } else if (p.out_dtype == ISB_BF16 && tv == 32) {
+        } else if (p.out_dtype == ISB_BF16 && tv == 32 && (p.dbg & 16)) {  // A/B: previous form
           __nv_bfloat16* po = static_cast<__nv_bfloat16*>(p.out) + mb * p.N + n;
 #pragma unroll
           for (int t = 0; t < 32; ++t) {
             const double o = static_cast<double>(static_cast<int32_t>(v[t])) * sa_t[cc + t];
-            // streaming store: the output is written once and must not evict the
-            // activation tiles every N-tile CTA re-reads from L2
             const uint16_t b = __bfloat16_as_ushort(__float2bfloat16_rn(__double2float_rn(o)));
             asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(po + static_cast<int64_t>(t) * p.N), "h"(b)
                          : "memory");
+          }
+        } else if ((p.out_dtype == ISB_BF16 || p.out_dtype == ISB_F16) && tv == 32) {
+          // Eq. 2 (gemm.cpp:252) for 32 tokens: (double)acc via the 2^52 + 2^31 bias (a DADD
+          // on the FP64 pipe instead of an I2F.F64 conversion), one DMUL, one F2F.F32.F64;
+          // all 32 chains independent (no store in between), then lane pairs exchange one
+          // value so each lane stores two adjacent channels of one token as a 32-bit word.
+          float f[32];
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const double d = __hiloint2double(0x43300000, static_cast<int>(v[t] ^ 0x80000000u)) -
+                             4503601774854144.0;
+            f[t] = __double2float_rn(d * sa_t[cc + t]);
+          }
+          const bool pairs = (p.N % 2 == 0) && static_cast<int64_t>(nt) * kTileN + q * 32 + 32 <= p.N;
+          if (pairs) {
+            // even lane: token t, channels (n, n+1); odd lane: token t+1, channels (n-1, n)
+            const bool odd = lane & 1;
+            uint32_t* po = reinterpret_cast<uint32_t*>(static_cast<uint16_t*>(p.out) +
+                                                       (mb + (odd ? 1 : 0)) * p.N + (n - (odd ? 1 : 0)));
+#pragma unroll
+            for (int t = 0; t < 32; t += 2) {
+              const float x = __shfl_xor_sync(0xffffffffu, odd ? f[t] : f[t + 1], 1);
+              const float lo = odd ? x : f[t], hi = odd ? f[t + 1] : x;
+              uint32_t w;
+              if (p.out_dtype == ISB_BF16) {
+                const __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
+                w = *reinterpret_cast<const uint32_t*>(&b);
+              } else {
+                const __half2 b = __floats2half2_rn(lo, hi);
+                w = *reinterpret_cast<const uint32_t*>(&b);
+              }
+              // streaming store: written once, must not evict the L2-resident activations
+              asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(po + static_cast<int64_t>(t) * (p.N / 2)), "r"(w));
+            }
+          } else {
+            uint16_t* po = static_cast<uint16_t*>(p.out) + mb * p.N + n;
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+              const uint16_t b = p.out_dtype == ISB_BF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(f[t]))
+                                                         : __half_as_ushort(__float2half_rn(f[t]));
+              asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(po + static_cast<int64_t>(t) * p.N), "h"(b));
+            }
           }
         } else {
 #pragma unroll

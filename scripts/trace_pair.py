@@ -1,0 +1,75 @@
+"""Timeline of the CTA-pair prefill kernel (cluster 0, clock64): per 128-K block the MMA
+warp's a_full / xfull wait completion and issue end, the transform's wfull / a_empty
+waits, the epilogue's d_full / release. Usage: python trace_pair.py [M K N] [flags]"""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2405_14597_b200 as isb  # noqa: E402
+from paper_2405_14597_b200 import _lib  # noqa: E402
+
+m, k, n = (int(a) for a in sys.argv[1:4]) if len(sys.argv) > 3 else (2048, 4096, 22016)
+flags = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+dev = torch.device("cuda:0")
+gen = torch.Generator(device=dev)
+gen.manual_seed(0)
+wf = bench.llama_like_weight(k, n, gen, dev)
+codes, scales = isb.quantize_weight(wf, 128, 4)
+s = isb.integerize_scales(scales.cpu().numpy(), 1024)
+w = isb.PackedWeight.from_codes(codes, 128, scales, s.int_scales, 1024)
+q, sa = isb.quantize_per_token(torch.randn((m, k), device=dev))
+out = torch.empty((m, n), dtype=torch.bfloat16, device=dev)
+lib = _lib.load()
+lib.isb_debug_set_flags(flags)
+for _ in range(3):
+    isb.gemm_integer_scale(q, sa, w, out=out)
+torch.cuda.synchronize()
+tr = torch.zeros((32, 512), dtype=torch.int64, device=dev)
+lib.isb_debug_set_trace.argtypes = [C.c_void_p, C.c_int]
+lib.isb_debug_set_trace(C.c_void_p(tr.data_ptr()), 0)
+isb.gemm_integer_scale(q, sa, w, out=out)
+torch.cuda.synchronize()
+lib.isb_debug_set_trace(None, 0)
+lib.isb_debug_set_flags(0)
+t = tr.cpu().numpy()
+kb = k // 128
+nb = int((t[2] != 0).sum())
+t0 = t[2][0] - 1
+print(f"M={m} K={k} N={n} flags={flags:#x}: {nb} blocks traced on the leader MMA warp")
+iss = t[2][:nb]
+d = np.diff(iss)
+print(f"MMA issue-to-issue per block: median {np.median(d):.0f} cyc, mean {d.mean():.0f} "
+      f"(ideal 512 at 256 tokens, 384 at 192)")
+wa = t[0][1:nb] - t[2][:nb - 1]
+wx = t[1][1:nb] - t[0][1:nb]
+print(f"MMA waiting a_full after prev issue: median {np.median(wa):.0f}, mean {wa.mean():.0f}; "
+      f"then xfull: median {np.median(wx):.0f}, mean {wx.mean():.0f}")
+for r, lab in ((5, "leader xform arrive"), (21, "peer xform arrive")):
+    x = t[r][t[r] != 0]
+    if len(x) > 2:
+        dd = np.diff(x[:nb])
+        print(f"{lab:26s}: per-block interval median {np.median(dd):.0f}, mean {dd.mean():.0f}")
+ph = [t[r] for r in (8, 9, 10, 11, 12, 5)]
+ok = np.all([x != 0 for x in ph], axis=0)
+if ok.sum():
+    names = ["wfull->lds+release", "->fold done", "->a_empty ok", "->stores+fence", "->arrived"]
+    for i, nm in enumerate(names):
+        d = (ph[i + 1] - ph[i])[ok]
+        print(f"xform phase {nm:22s}: median {np.median(d):.0f} mean {d.mean():.0f}")
+    gap = (t[8][1:] - t[5][:-1])
+    w = np.nonzero(ok)[0]
+    st = np.diff(t[8][w])
+    print(f"xform iteration start-to-start (same warp): median {np.median(st):.0f}")
+print("first 12 blocks (rel. cycles): j, mma_afull, mma_xfull, mma_issued")
+for j in range(min(12, nb)):
+    print(j, *(int(t[r][j] - t0) if t[r][j] else -1 for r in (0, 1, 2)))
+ne = int((t[6] != 0).sum())
+for it in range(min(ne, 6)):
+    tile_end = t[2][(it + 1) * kb - 1] if (it + 1) * kb - 1 < nb else 0
+    print(f"tile {it}: last issue {tile_end - t0}, d_full seen {t[6][it] - t0}, released {t[7][it] - t0}, "
+          f"next first issue {t[2][(it + 1) * kb] - t0 if (it + 1) * kb < nb else -1}")
