@@ -263,8 +263,10 @@ void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
   if (fold_eligible(m, *w, path) && !fold_disabled()) {
     // 1-CTA SS kernel (gemm_fold.cu) by default; debug flag kDbgPair selects the CTA-pair
     // experiment (gemm_pair.cu) for A/B measurements in one process.
-    if (g_dbg & kDbgPair)
-      launch_gemm_pair(xq, sa, m, *w, out, out_dtype, num_sms(), as_stream(stream));
+    // M >= 512: CTA-pair kernel with tokens as the MMA M (gemm_sp.cu); below, the 1-CTA
+    // SS kernel (gemm_fold.cu; debug flag kDbgFoldSS forces it for A/B measurements).
+    if (m >= kSpMinM && !(g_dbg & kDbgFoldSS))
+      launch_gemm_sp(xq, sa, m, *w, out, out_dtype, num_sms(), as_stream(stream));
     else
       launch_gemm_fold(xq, sa, m, *w, out, out_dtype, num_sms(), as_stream(stream));
     return;

@@ -923,7 +923,14 @@ struct GroupPlan {
   unsigned* sync_dev = nullptr;
   uint32_t* partials = nullptr;
   void* owned = nullptr;      // plan-owned codes / scales when the caller passes none
+  // Prefill route (every problem M >= kSpMinM, integer scale, k_g <= 16): K1 per problem
+  // (when float activations are given) + one grouped CTA-pair fold launch (gemm_sp.cu).
+  SpGroupPlan* sp = nullptr;
+  isb_group_problem sp_probs[8] = {};  // resolved codes / scales pointers
+  int sp_n = 0;
+  int sp_x_dtype[8] = {};
   ~GroupPlan() {
+    if (sp) sp_group_destroy(sp);
     if (sched_dev) cudaFree(sched_dev);
     if (sync_dev) cudaFree(sync_dev);
     if (partials) cudaFree(partials);
@@ -1017,10 +1024,34 @@ GroupPlan* group_plan_create(const isb_group_problem* probs, int nprob, int path
     }
   }
   if (quantize < 0) quantize = 0;
+  bool prefill = path == ISB_PATH_INTEGER_SCALE;
+  for (int i = 0; i < nprob && prefill; ++i)
+    prefill = probs[i].m >= kSpMinM && fold_eligible(probs[i].m, *probs[i].w, path);
   auto* pl = new GroupPlan();
   try {
     cuda_check(cudaGetDevice(&pl->dev), "cudaGetDevice");
     pl->path = path;
+    if (prefill) {
+      if (own_bytes) cuda_check(cudaMalloc(&pl->owned, own_bytes), "cudaMalloc(group workspace)");
+      uint8_t* own = static_cast<uint8_t*>(pl->owned);
+      pl->prm.quantize = quantize;
+      for (int i = 0; i < nprob; ++i) {
+        isb_group_problem q = probs[i];
+        if (quantize) {
+          if (!q.xq) { q.xq = reinterpret_cast<int8_t*>(own); own += (q.m * q.w->k + 255) / 256 * 256; }
+          if (!q.sa) { q.sa = reinterpret_cast<double*>(own); own += (q.m * 8 + 255) / 256 * 256; }
+          pl->sp_x_dtype[i] = q.x_dtype;
+        }
+        pl->sp_probs[pl->sp_n++] = q;
+      }
+      cuda_check(cudaMalloc(&pl->sync_dev, kSyncWords * sizeof(unsigned)), "cudaMalloc(group sync)");
+      cuda_check(cudaMemset(pl->sync_dev, 0, kSyncWords * sizeof(unsigned)), "cudaMemset(group sync)");
+      pl->sp = sp_group_create(pl->sp_probs, nprob, out_dtype, num_sms);
+      pl->grid = 2 * (num_sms / 2);
+      pl->mt = kSpTileTokens;
+      pl->makespan = 1.0 / std::max(1e-9, sp_group_balance(pl->sp));
+      return pl;
+    }
     pl->mt = pick_group_mt(max_m);
     const int mt = pl->mt;
     const int S = 4;  // Cfg<16/32>::S
@@ -1175,6 +1206,16 @@ void group_plan_run(GroupPlan* pl, cudaStream_t s) {
   int dev = 0;
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   if (dev != pl->dev) fail(ISB_PARAM, "grouped GEMM plan used on another device");
+  if (pl->sp) {
+    if (pl->prm.quantize)
+      for (int i = 0; i < pl->sp_n; ++i) {
+        const isb_group_problem& q = pl->sp_probs[i];
+        launch_quantize_per_token(q.x, pl->sp_x_dtype[i], q.m, q.w->k, q.xq, q.sa,
+                                  reinterpret_cast<int*>(pl->sync_dev + kSyncBad), s);
+      }
+    sp_group_run(pl->sp, s);
+    return;
+  }
   if (pl->mt == 16) {
     if (pl->path == ISB_PATH_INTEGER_SCALE)
       launch_group_mt<16, ISB_PATH_INTEGER_SCALE>(pl->maps, pl->prm, pl->grid, s);

@@ -89,17 +89,17 @@ constexpr int64_t kFoldMinM = 256;
 bool fold_eligible(int64_t m, const isb_weight& w, int path);
 void launch_gemm_fold(const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                       void* out, int out_dtype, int num_sms, cudaStream_t s);
-// Prefill K3 fold on a CTA pair (gemm_pair.cu): experiment, selected by a debug flag.
-constexpr int kDbgPair = 1 << 21;  // isb_debug_set_flags: use gemm_pair.cu instead of gemm_fold.cu
-int pair_tile_tokens();
-void launch_gemm_pair(const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
-                      void* out, int out_dtype, int num_sms, cudaStream_t s);
-struct PairGroupPlan;
-PairGroupPlan* pair_group_create(const isb_group_problem* probs, int nprob, int out_dtype,
-                                 int num_sms);
-void pair_group_run(PairGroupPlan* pl, cudaStream_t s);
-double pair_group_efficiency(const PairGroupPlan* pl);
-void pair_group_destroy(PairGroupPlan* pl);
+// Prefill K3 fold, CTA pair with tokens as the MMA M (gemm_sp.cu).
+constexpr int kDbgFoldSS = 1 << 22;  // isb_debug_set_flags: force gemm_fold.cu at M >= 512 (A/B)
+constexpr int64_t kSpMinM = 512;   // one pair tile = 512 tokens
+constexpr int kSpTileTokens = 512;
+void launch_gemm_sp(const int8_t* xq, const double* sa, int64_t m, const isb_weight& w, void* out,
+                    int out_dtype, int num_sms, cudaStream_t s);
+struct SpGroupPlan;
+SpGroupPlan* sp_group_create(const isb_group_problem* probs, int nprob, int out_dtype, int num_sms);
+void sp_group_run(SpGroupPlan* pl, cudaStream_t s);
+double sp_group_balance(const SpGroupPlan* pl);
+void sp_group_destroy(SpGroupPlan* pl);
 // Prefill per-group-epilogue K3 (any k_g) / K4 on the SS skeleton (gemm_pg.cu).
 constexpr int64_t kPgMinM = 128;
 bool pg_eligible(int64_t m, const isb_weight& w);

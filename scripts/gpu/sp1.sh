@@ -1,0 +1,1 @@
+ISB_AB_FLAG=4194304 timeout 100 python scripts/pair_quick.py 2048 1 4 5 2>&1

@@ -1,5 +1,5 @@
-"""Prefill fold: CTA-pair experiment (gemm_pair.cu, debug flag 1<<21) vs the 1-CTA SS kernel
-(gemm_fold.cu, default) on the LLaMA-2-7B layer at M (default 2048): bit-identical outputs
+"""Prefill fold: the CTA-pair kernel (gemm_sp.cu, default at M >= 512) vs the 1-CTA SS kernel
+(gemm_fold.cu, forced with debug flag 1<<22) on the LLaMA-2-7B layer at M (default 2048): bit-identical outputs
 (int32 / bf16) and per-linear kernel times. python pair_quick.py [M] [extra flags...]"""
 import os
 import sys
@@ -11,8 +11,8 @@ import bench  # noqa: E402
 import paper_2405_14597_b200 as isb  # noqa: E402
 from paper_2405_14597_b200 import _lib  # noqa: E402
 
-SS = 0
-PAIR = 1 << 21
+SS = 1 << 22
+PAIR = 0
 dev = torch.device("cuda:0")
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
 extra = [int(a) for a in sys.argv[2:]]

@@ -13,6 +13,9 @@ m, k, n = (int(a) for a in sys.argv[1:4])
 path = sys.argv[4] if len(sys.argv) > 4 else "int"
 iters = int(sys.argv[5]) if len(sys.argv) > 5 else 6
 dev = torch.device("cuda:0")
+if os.environ.get('ISB_AB_FLAG'):
+    from paper_2405_14597_b200 import _lib
+    _lib.load().isb_debug_set_flags(int(os.environ['ISB_AB_FLAG']))
 gen = torch.Generator(device=dev)
 gen.manual_seed(0)
 ws = []

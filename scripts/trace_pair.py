@@ -25,7 +25,7 @@ w = isb.PackedWeight.from_codes(codes, 128, scales, s.int_scales, 1024)
 q, sa = isb.quantize_per_token(torch.randn((m, k), device=dev))
 out = torch.empty((m, n), dtype=torch.bfloat16, device=dev)
 lib = _lib.load()
-lib.isb_debug_set_flags(flags)
+lib.isb_debug_set_flags(flags | int(os.environ.get('ISB_AB_FLAG', 0)))
 for _ in range(3):
     isb.gemm_integer_scale(q, sa, w, out=out)
 torch.cuda.synchronize()
@@ -68,6 +68,11 @@ if ok.sum():
 print("first 12 blocks (rel. cycles): j, mma_afull, mma_xfull, mma_issued")
 for j in range(min(12, nb)):
     print(j, *(int(t[r][j] - t0) if t[r][j] else -1 for r in (0, 1, 2)))
+e8, e9, e10, e11 = t[8], t[9], t[10], t[11]
+okc = (e8 != 0) & (e9 != 0) & (e10 != 0) & (e11 != 0)
+if okc.sum() > 4:
+    print(f"epilogue chunk (warp 0): tmem ld {np.median((e9 - e8)[okc]):.0f}, convert {np.median((e10 - e9)[okc]):.0f}, "
+          f"pack+stage+store {np.median((e11 - e10)[okc]):.0f}, next chunk start {np.median((e8[1:] - e11[:-1])[okc[:-1] & (e8[1:] != 0)]):.0f} (medians, cycles)")
 ne = int((t[6] != 0).sum())
 for it in range(min(ne, 6)):
     tile_end = t[2][(it + 1) * kb - 1] if (it + 1) * kb - 1 < nb else 0

@@ -97,7 +97,8 @@ def check_int_all_dtypes(x, w, s, ref, pw, repeats=0):
 
 
 # ------------------------------------------------------------------------- prefill, many tiles
-PREFILL_MANY = [(2048, 512, 4096), (2048, 4096, 4096), (1536, 1024, 11008), (2048, 1024, 640)]
+PREFILL_MANY = [(2048, 512, 4096), (2048, 4096, 4096), (1536, 1024, 11008), (2048, 1024, 640),
+                (1000, 512, 4096), (700, 1024, 1000)]
 
 
 @pytest.mark.parametrize("m,k,n", PREFILL_MANY)
@@ -107,8 +108,28 @@ def test_prefill_fold_more_tiles_than_sms(m, k, n):
     assert s.int_scales.max() <= 16  # the folded (default prefill) kernel
     ref = O.gemm_integer_scale(x, w, s, workers=os.cpu_count() or 1)
     check_int_all_dtypes(x, w, s, ref, pack(w, s), repeats=50)
-    if (m, k, n) != (2048, 1024, 640):
+    if (m, k, n) in PREFILL_MANY[:3]:
         assert tiles > NSM, f"{tiles} tiles: want more than {NSM} SMs"
+
+
+def test_prefill_pair_kernel_equals_one_cta_kernel():
+    """M >= 512 runs the CTA-pair kernel (gemm_sp.cu); the 1-CTA SS kernel (gemm_fold.cu,
+    forced by debug flag 1 << 22) must give identical int32 / bf16 / f32 results,
+    including ragged M and N (M % 512, N % 128 != 0)."""
+    lib = isb._lib.load()
+    for m, k, n in [(2048, 1024, 4096), (1111, 512, 1000), (512, 256, 128)]:
+        x, w, s, _, _ = llama_problem(m, k, n, seed_w=900 + n, seed_x=950 + m)
+        pw = pack(w, s)
+        xq, sa = dev(x.values, torch.int8), dev(x.scales)
+        for dt in (torch.int32, torch.float32, torch.bfloat16, torch.float16):
+            a = isb.gemm_integer_scale(xq, sa, pw, out_dtype=dt)
+            lib.isb_debug_set_flags(1 << 22)
+            try:
+                b = isb.gemm_integer_scale(xq, sa, pw, out_dtype=dt)
+            finally:
+                lib.isb_debug_set_flags(0)
+            torch.cuda.synchronize()
+            assert torch.equal(a, b), f"pair != 1-CTA at {(m, k, n)} {dt}"
 
 
 @pytest.mark.parametrize("m,k,n", [(2048, 512, 4096), (1024, 1024, 2560)])
