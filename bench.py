@@ -402,6 +402,26 @@ def grouped_layer_us(isb, layers, xs, path, iters=100):
     return e0.elapsed_time(e1) * 1e3 / iters, plans[0]
 
 
+def grouped_prefill_us(isb, layers, xq_sa, iters=8):
+    """Device time of the layer's four integer-scale GEMMs at prefill M as ONE grouped
+    launch (isb_group_plan with pre-quantized codes: the CTA-pair fold kernel, tiles of
+    all four linears dealt longest-first over the SM pairs), graph of `iters` launches
+    rotating the weight replicas."""
+    import torch
+    plans = [isb.GroupedGemm([{"weight": l[3], "xq": q, "sa": sa}
+                              for l, (q, sa) in zip(layers[r], xq_sa)])
+             for r in range(REPLICAS)]
+    g = graph_of([lambda: [plans[i % REPLICAS].run() for i in range(iters)]])[0]
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / iters, plans[0]
+
+
 def run_ours(args, ws, rank, local):
     import numpy as np
     import torch
@@ -515,11 +535,19 @@ def run_ours(args, ws, rank, local):
                 xq = [isb.quantize_per_token(torch.randn((mm, k), device=dev)) for _, k, _ in LAYER]
                 ti = gemm_kernel_timing(isb, layers, xq, mm, "int", iters=10)
                 tf = gemm_kernel_timing(isb, layers, xq, mm, "float", iters=10)
-                us_i = sum(r["us"] for r in ti)
+                us_pl = sum(r["us"] for r in ti)
                 us_f = sum(r["us"] for r in tf)
                 byts = sum(r["alg_bytes"] for r in ti)
-                row["kernel"] = "per-linear prefill kernels (int: k_g-folded SS-256, float: MT=128)"
                 row["per_linear_int"] = ti
+                row["us_per_layer_int_per_linear_launches"] = round(us_pl, 2)
+                if mm >= 512:
+                    us_i, gpl = grouped_prefill_us(isb, layers, xq)
+                    row["kernel"] = ("int: grouped prefill launch of the 4 linears (k_g-folded "
+                                     "CTA-pair kernel gemm_w4a8_sp, 512-token x 128-channel pair "
+                                     "tiles, LPT); float: per-linear per-group-epilogue kernel")
+                else:
+                    us_i = us_pl
+                    row["kernel"] = "per-linear prefill kernels (int: k_g-folded SS-256, float: per-group)"
             row.update({"us_per_layer_int": round(us_i, 2), "us_per_layer_float": round(us_f, 2),
                         "speedup_vs_float": round(us_f / us_i, 3),
                         "us_per_layer_fp16_dense": round(us_d, 2),
@@ -546,7 +574,9 @@ def run_ours(args, ws, rank, local):
                                "peak": 4786.0, "peak_kind": "measured tcgen05 kind::i8 (r01_mma_peak)",
                                "unit": "TOPS", "frac": round(ops / us_i / 1e6 / 4786.0, 4),
                                "frac_nominal_4500": round(ops / us_i / 1e6 / 4500.0, 4),
-                               "kernel": "gemm_w4a8_fold_ss<256> per linear, M=2048 layer"}
+                               "kernel": "gemm_w4a8_sp (CTA pair, k_g folded), grouped launch of "
+                                         "the LLaMA-2-7B layer's 4 linears, M=2048",
+                               "per_linear_launches_us": round(us_pl, 2)}
 
     moe_res = None
     if not args.no_moe:
