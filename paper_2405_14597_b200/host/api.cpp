@@ -86,11 +86,8 @@ void validate_activation(const QuantizedTensor& x) {
     throw ValueError("activation codes outside max-based symmetric range");
 }
 
-// gemm.cpp:119-134
-Index validate_grouped_weight(const QuantizedTensor& x, const QuantizedTensor& w) {
-  if (x.cols() != w.rows())
-    throw DimensionError("activation K=" + std::to_string(x.cols()) + " vs weight rows " +
-                         std::to_string(w.rows()));
+// gemm.cpp:119-134 (the weight part)
+Index validate_weight(const QuantizedTensor& w) {
   if (w.params.scheme != Scheme::symmetric) throw ParamError("weights must be symmetric");
   const GranKind kind = w.params.granularity.kind;
   if (kind != GranKind::group && kind != GranKind::per_channel)
@@ -105,6 +102,14 @@ Index validate_grouped_weight(const QuantizedTensor& x, const QuantizedTensor& w
     throw ParamError("the B200 path packs 4-bit weights (W4A8); got " +
                      std::to_string(w.params.bit_width) + "-bit");
   return g;
+}
+
+// gemm.cpp:119-134
+Index validate_grouped_weight(const QuantizedTensor& x, const QuantizedTensor& w) {
+  if (x.cols() != w.rows())
+    throw DimensionError("activation K=" + std::to_string(x.cols()) + " vs weight rows " +
+                         std::to_string(w.rows()));
+  return validate_weight(w);
 }
 
 // Device operands of one GEMM call.
@@ -542,5 +547,72 @@ GemmResult run_layer(const QuantizedTensor& x, const QuantizedTensor& w, const P
       throw ParamError("path '" + to_string(path.kind) + "' is outside the B200 integer-scale path");
   }
 }
+
+// ---------------------------------------------------------------------------
+// Device-resident entry points (include/intscale/gemm.hpp, namespace device).
+namespace device {
+
+PackedWeight::PackedWeight(const QuantizedTensor& w, const IntegerScaleSet* int_scales, void* stream) {
+  const Index g = validate_weight(w);
+  const Index k = w.rows(), n = w.cols(), groups = k / g;
+  Dev codes(static_cast<std::size_t>(k * n) * 2), scales(static_cast<std::size_t>(n * groups) * 8),
+      ks(int_scales ? static_cast<std::size_t>(n * groups) * 4 : 0);
+  up(codes, w.values.data(), static_cast<std::size_t>(k * n));
+  up(scales, w.params.scales.data(), static_cast<std::size_t>(n * groups));
+  if (int_scales) {
+    if (int_scales->int_scales.size() != n * groups)
+      throw ParamError("integer scale count does not match the weight's groups");
+    up(ks, int_scales->int_scales.data(), static_cast<std::size_t>(n * groups));
+  }
+  check(isb_weight_pack_codes(codes.as<std::int16_t>(), k, n, g, scales.as<double>(),
+                              int_scales ? ks.as<std::int32_t>() : nullptr,
+                              int_scales ? int_scales->amplifier : 1, stream, &h_));
+  // the packer reads its inputs asynchronously: keep them alive until it has run
+  cuda(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "pack");
+  k_ = k;
+  n_ = n;
+}
+
+PackedWeight::~PackedWeight() { isb_weight_destroy(h_); }
+
+PackedWeight::PackedWeight(PackedWeight&& o) noexcept : h_(o.h_), k_(o.k_), n_(o.n_) {
+  o.h_ = nullptr;
+}
+
+PackedWeight& PackedWeight::operator=(PackedWeight&& o) noexcept {
+  if (this != &o) {
+    isb_weight_destroy(h_);
+    h_ = o.h_;
+    k_ = o.k_;
+    n_ = o.n_;
+    o.h_ = nullptr;
+  }
+  return *this;
+}
+
+void quantize_per_token(const float* x, Activations& out, void* stream) {
+  check(isb_quantize_per_token(x, ISB_F32, out.m, out.k, out.codes, out.scales, 0, stream));
+}
+
+std::size_t workspace_bytes(Index m, const PackedWeight& w) {
+  std::int64_t b = 0;
+  check(isb_gemm_workspace_size(m, w.handle(), &b));
+  return static_cast<std::size_t>(b);
+}
+
+void gemm_integer_scale(const Activations& x, const PackedWeight& w, void* out, OutType type,
+                        void* workspace, std::size_t ws_bytes, void* stream) {
+  check(isb_gemm_integer_scale(x.codes, x.scales, x.m, x.k, w.handle(), out,
+                               static_cast<int>(type), workspace,
+                               static_cast<std::int64_t>(ws_bytes), stream));
+}
+
+void gemm_float_scale(const Activations& x, const PackedWeight& w, void* out, OutType type,
+                      void* workspace, std::size_t ws_bytes, void* stream) {
+  check(isb_gemm_float_scale(x.codes, x.scales, x.m, x.k, w.handle(), out, static_cast<int>(type),
+                             workspace, static_cast<std::int64_t>(ws_bytes), stream));
+}
+
+}  // namespace device
 
 }  // namespace intscale

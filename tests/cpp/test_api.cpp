@@ -7,7 +7,10 @@
 #include <intscale/quantize.hpp>
 #include <intscale/tensor_io.hpp>
 
+#include <cuda_runtime.h>
 #include <unistd.h>
+
+#include <algorithm>
 
 #include <bit>
 #include <cmath>
@@ -328,16 +331,78 @@ static void test_tensor_core_layer() {
   auto w = quantize(wf, 4, Scheme::symmetric, Granularity::group_of(128));
   auto x = quantize(xf, 8, Scheme::symmetric, Granularity::per_token());
   auto set = integerize_scales(w.params.scales, search_amplifier(w.params.scales));
-  auto r = gemm_integer_scale(x, w, set);  // throws if tcgen05 and int64 outputs differ
+  GemmOptions stats;
+  stats.track_accumulator = true;  // opt-in second pass: tcgen05 output checked against int64
+  auto r = gemm_integer_scale(x, w, set, stats);  // throws if tcgen05 and int64 outputs differ
   CHECK(r.stats.tensor_core);
   CHECK(r.stats.max_abs_accumulator > 0);
-  GemmOptions fast;
-  fast.track_accumulator = false;
-  auto r2 = gemm_integer_scale(x, w, set, fast);
+  auto r2 = gemm_integer_scale(x, w, set);  // default: tcgen05 only
   CHECK(r2.output == r.output);
   CHECK(r2.stats.max_abs_accumulator == -1);
 }
 
+
+// Device-resident overloads (include/intscale/gemm.hpp, namespace device): weight packed
+// once, activations quantized and consumed in HBM, results equal the host-matrix calls.
+static void test_device_entry_points() {
+  std::mt19937_64 rng(7);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  const Index m = 40, k = 512, n = 384;
+  MatF wf(k, n), xf(m, k);
+  for (Index i = 0; i < k * n; ++i) wf.data()[i] = static_cast<float>(0.02 * u(rng));
+  for (Index i = 0; i < m * k; ++i) xf.data()[i] = static_cast<float>(2.0 * u(rng));
+  auto w = quantize(wf, 4, Scheme::symmetric, Granularity::group_of(128));
+  auto x = quantize(xf, 8, Scheme::symmetric, Granularity::per_token());
+  auto set = integerize_scales(w.params.scales, 1024);
+  const auto host_i = gemm_integer_scale(x, w, set);
+  const auto host_f = gemm_float_scale(x, w);
+
+  device::PackedWeight pw(w, &set);
+  CHECK(pw.k() == k && pw.n() == n);
+  float* xd = nullptr;
+  device::Activations xa;
+  xa.m = m;
+  xa.k = k;
+  void *out = nullptr, *ws = nullptr;
+  const std::size_t wsb = std::max<std::size_t>(256, device::workspace_bytes(m, pw));
+  cudaMalloc(reinterpret_cast<void**>(&xd), m * k * 4);
+  cudaMalloc(reinterpret_cast<void**>(&xa.codes), m * k);
+  cudaMalloc(reinterpret_cast<void**>(&xa.scales), m * 8);
+  cudaMalloc(&out, m * n * 4);
+  cudaMalloc(&ws, wsb);
+  cudaMemset(ws, 0, wsb);
+  cudaMemcpy(xd, xf.data(), m * k * 4, cudaMemcpyHostToDevice);
+  device::quantize_per_token(xd, xa);
+  std::vector<std::int8_t> codes(m * k);
+  std::vector<double> scales(m);
+  cudaMemcpy(codes.data(), xa.codes, m * k, cudaMemcpyDeviceToHost);
+  cudaMemcpy(scales.data(), xa.scales, m * 8, cudaMemcpyDeviceToHost);
+  bool same_codes = true;
+  for (Index i = 0; i < m * k; ++i) same_codes &= codes[i] == x.values.data()[i];
+  CHECK(same_codes);
+  CHECK(std::equal(scales.begin(), scales.end(), x.params.scales.data()));
+  MatF y(m, n);
+  device::gemm_integer_scale(xa, pw, out, device::OutType::f32, ws, wsb);
+  cudaMemcpy(y.data(), out, m * n * 4, cudaMemcpyDeviceToHost);
+  CHECK(y == host_i.output);  // bit-identical
+  device::gemm_float_scale(xa, pw, out, device::OutType::f32, ws, wsb);
+  cudaMemcpy(y.data(), out, m * n * 4, cudaMemcpyDeviceToHost);
+  double mag = 0.0, e2 = 0.0;
+  for (Index i = 0; i < m * n; ++i) mag = std::max(mag, std::abs(double(host_f.output.data()[i])));
+  for (Index i = 0; i < m * n; ++i)
+    e2 = std::max(e2, std::abs(double(y.data()[i]) - double(host_f.output.data()[i])));
+  CHECK(e2 <= 1e-4 * mag);  // fp32 group accumulation vs the reference's double
+  device::PackedWeight moved = std::move(pw);
+  CHECK(moved.handle() != nullptr && pw.handle() == nullptr);
+  CHECK_THROWS_AS(device::gemm_integer_scale(xa, device::PackedWeight(w), out, device::OutType::f32,
+                                             ws, wsb),
+                  ParamError);  // no integer scales packed
+  cudaFree(xd);
+  cudaFree(xa.codes);
+  cudaFree(xa.scales);
+  cudaFree(out);
+  cudaFree(ws);
+}
 
 // ------------------------------------------------------------------ QTNS container
 namespace fs = std::filesystem;
@@ -614,6 +679,7 @@ int main() {
       {"overflow_bound_pins", test_overflow_bound_pins},
       {"dyadic_agreement", test_dyadic_agreement},
       {"tensor_core_layer", test_tensor_core_layer},
+      {"device_entry_points", test_device_entry_points},
       {"coarse_equals_integer_at_alpha", test_coarse_equals_integer_at_alpha},
       {"coarse_tensor_core", test_coarse_tensor_core},
       {"qtns_containers", test_qtns_containers},
