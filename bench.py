@@ -795,6 +795,123 @@ def cpu_baseline(args):
                               "cores": threads, "nproc": nproc, "cpu": model}}
 
 
+
+# ----------------------------------------------------------------------------- tensor parallel
+# BASELINE configs[3] (C4): LLaMA-2-70B decoder-layer linears across N GPUs, Megatron
+# layout — qkv / gate_up column-parallel (N-split; their outputs stay sharded for the
+# head-parallel attention / the sharded SwiGLU), o / down row-parallel (K-split on group
+# boundaries: per-token scale from an all-reduce MAX of partial row maxima, raw int32
+# accumulator, exact all-reduce SUM in int32, one Eq. 2 epilogue; parallel.py).
+LAYER_70B = [("qkv_proj", 8192, 10240, "col"), ("o_proj", 8192, 8192, "row"),
+             ("gate_up_proj", 8192, 57344, "col"), ("down_proj", 28672, 8192, "row")]
+
+
+def run_tp(args, ws, rank, local):
+    import torch
+    import paper_2405_14597_b200 as isb
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    m = args.m
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4321 + rank)
+    lin = []
+    for name, k, n, kind in LAYER_70B:
+        ks, ns = (k, n // ws) if kind == "col" else (k // ws, n)
+        assert ks % GROUP == 0 and ns % 128 == 0, (name, ks, ns)
+        wf = llama_like_weight(ks, ns, gen, dev)
+        codes, scales = isb.quantize_weight(wf, GROUP, 4)
+        del wf
+        si = isb.integerize_scales(scales.cpu().numpy(), ALPHA)
+        w = isb.PackedWeight.from_codes(codes, GROUP, scales, si.int_scales, ALPHA)
+        x = torch.randn((m, ks), generator=gen, device=dev)   # replicated (col) / K-slice (row)
+        lin.append((name, k, n, kind, ks, ns, w, x))
+    wsp = isb.Workspace()
+    rows = [l for l in lin if l[3] == "row"]
+    # both row-parallel linears' partial maxima / int32 accumulators live in ONE buffer each,
+    # so a step needs one all-reduce MAX and one all-reduce SUM
+    amax_all = torch.empty((len(rows), m), dtype=torch.float32, device=dev)
+    acc_all = torch.empty((sum(m * l[5] for l in rows),), dtype=torch.int32, device=dev)
+    bufs, off = {}, 0
+    for name, k, n, kind, ks, ns, w, x in lin:
+        b = {"xq": torch.empty((m, ks), dtype=torch.int8, device=dev),
+             "sa": torch.empty((m,), dtype=torch.float64, device=dev),
+             "out": torch.empty((m, ns), dtype=torch.bfloat16, device=dev)}
+        if kind == "row":
+            b["acc"] = acc_all[off:off + m * ns].view(m, ns)
+            off += m * ns
+        bufs[name] = b
+    for i, l in enumerate(rows):
+        bufs[l[0]]["amax"] = amax_all[i]
+
+    cols = [l for l in lin if l[3] == "col"]
+    # the column linears (K1 fused) and the row linears (pre-quantized, raw int32
+    # accumulators) each run as ONE grouped launch (isb_group_plan)
+    col_plan = isb.GroupedGemm([{"weight": l[6], "x": l[7], "xq": bufs[l[0]]["xq"],
+                                 "sa": bufs[l[0]]["sa"], "out": bufs[l[0]]["out"]} for l in cols])
+    row_plan = isb.GroupedGemm([{"weight": l[6], "xq": bufs[l[0]]["xq"], "sa": bufs[l[0]]["sa"],
+                                 "out": bufs[l[0]]["acc"]} for l in rows], out_dtype=torch.int32)
+
+    def seg_local():      # column linears (K1 + K3), partial row maxima of the row linears
+        col_plan.run()
+        for name, k, n, kind, ks, ns, w, x in rows:
+            b = bufs[name]
+            isb.row_absmax(x, out=b["amax"])
+
+    def seg_row_gemm():   # quantize with the global maxima, raw int32 accumulators
+        for name, k, n, kind, ks, ns, w, x in rows:
+            b = bufs[name]
+            isb.quantize_per_token_amax(x, b["amax"], codes=b["xq"], scales=b["sa"])
+        row_plan.run()
+
+    def seg_finalize():   # one Eq. 2 epilogue per reduced accumulator
+        for name, k, n, kind, ks, ns, w, x in rows:
+            b = bufs[name]
+            isb.finalize_acc(b["acc"], b["sa"], ALPHA, out=b["out"])
+
+    graphs = graph_of([seg_local, seg_row_gemm, seg_finalize])
+
+    def step(collectives):
+        graphs[0].replay()
+        if collectives and ws > 1:
+            import torch.distributed as dist
+            dist.all_reduce(amax_all, op=dist.ReduceOp.MAX)
+        graphs[1].replay()
+        if collectives and ws > 1:
+            import torch.distributed as dist
+            dist.all_reduce(acc_all, op=dist.ReduceOp.SUM)
+        graphs[2].replay()
+
+    ops = sum(2 * m * k * n for _, k, n, _ in LAYER_70B)   # the whole layer, all ranks
+    res = {}
+    for mode in ("with_collectives", "compute_only"):
+        fn = (lambda i, c=(mode == "with_collectives"): step(c))
+        ms = max_over_ranks(time_steps(fn, args.steps, args.warmup, ws), ws) / args.steps
+        res[mode] = ms
+    us = res["with_collectives"] * 1e3
+    return {
+        "metric": METRIC, "value": round(ops / us / 1e6, 3), "unit": "TOPS", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["with_collectives"], 5),
+        "us_per_layer": round(us, 2), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int8 (s8 x s4->s8 MMA, s32 accumulate)",
+        "data": "synthetic (llama_like-structured int4 weights per shard, gaussian activations)",
+        "config": {"workload": f"llama2-70b decoder-layer linears, tensor-parallel tp{ws}, M={m}",
+                   "M": m, "parallelism": f"tp{ws} (Megatron: qkv/gate_up column-parallel, "
+                                          "o/down row-parallel, exact int32 all-reduce)",
+                   "linears": [{"name": a, "K": k, "N": n, "split": kind,
+                                "shard_K": (k if kind == "col" else k // ws),
+                                "shard_N": (n // ws if kind == "col" else n)}
+                               for a, k, n, kind in LAYER_70B],
+                   "group": GROUP, "alpha": ALPHA},
+        "compute_only_us_per_layer": round(res["compute_only"] * 1e3, 2),
+        "collective_us_per_layer": round((res["with_collectives"] - res["compute_only"]) * 1e3, 2),
+        "launches": "per step: 3 CUDA graphs (one grouped launch of the column linears with K1 "
+                    "fused + the row linears' partial maxima | amax-quantize + one grouped "
+                    "int32 launch of the row linears | Eq. 2 finalize) with, when N > 1, one "
+                    "NCCL all-reduce MAX (both row linears' maxima) and one all-reduce SUM "
+                    "(both int32 accumulators) between",
+        "gpu_launches": args.steps * 10,
+    }
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -806,6 +923,9 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-moe", action="store_true")
+    ap.add_argument("--mode", default="layer", choices=["layer", "tp"],
+                    help="layer: the headline (one grouped LLaMA-2-7B layer launch per step, "
+                         "replicated per GPU); tp: LLaMA-2-70B layer linears tensor-parallel")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -828,6 +948,14 @@ def main():
         return
 
     ws, rank, local = init_dist()
+    if args.mode == "tp":
+        res = run_tp(args, ws, rank, local)
+        if rank == 0:
+            print(json.dumps(res))
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     res = run_ours(args, ws, rank, local)
     if rank == 0:
         if ws == 1 and not args.no_cpu:

@@ -33,35 +33,68 @@ __device__ __forceinline__ float block_max256(float v, float* red) {
   return red[0];
 }
 
-// One CTA per row: max |x| over the (local slice of the) row. Exact (max).
+// Rows are split into kChunk-element chunks, one CTA per (chunk, row): decode-sized M
+// (16 rows of a 28672-wide slice) still spreads over ~100 SMs instead of 16.
+constexpr int kChunk = kThreads * 16;
+
+// max |x| over the (local slice of the) row: per-CTA max, then an atomic max on the
+// float bits into amax (zeroed by the launcher; non-negative floats order as integers).
+// NaNs are ignored (fmaxf), as in the one-CTA form.
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
-    row_absmax_kernel(const T* __restrict__ x, int64_t k, float* __restrict__ amax) {
+    row_absmax_kernel(const T* __restrict__ x, int64_t k, float* __restrict__ amax, bool vec) {
   __shared__ float red[kThreads / 32];
-  const T* xr = x + static_cast<int64_t>(blockIdx.x) * k;
+  const int64_t row = blockIdx.y;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kChunk;
+  const T* xr = x + row * k;
   if (threadIdx.x == 0) pdl_launch_dependents();
   pdl_wait();
   float m = 0.0f;
-  for (int64_t e = threadIdx.x; e < k; e += kThreads) m = fmaxf(m, fabsf(load1<T>(xr + e)));
+  if (vec) {
+    for (int64_t e = c0 + threadIdx.x * 4; e < min(k, c0 + kChunk); e += kThreads * 4) {
+      float v[4];
+      load4<T>(xr + e, v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) m = fmaxf(m, fabsf(v[i]));
+    }
+  } else {
+    for (int64_t e = c0 + threadIdx.x; e < min(k, c0 + kChunk); e += kThreads)
+      m = fmaxf(m, fabsf(load1<T>(xr + e)));
+  }
   m = block_max256(m, red);
-  if (threadIdx.x == 0) amax[blockIdx.x] = m;
+  if (threadIdx.x == 0) atomicMax(reinterpret_cast<int*>(amax) + row, __float_as_int(m));
 }
 
-// One CTA per row: K1 with the row max supplied (the all-reduced global max).
+// K1 with the row max supplied (the all-reduced global max), one CTA per (chunk, row).
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
     quantize_amax_kernel(const T* __restrict__ x, int64_t k, const float* __restrict__ amax,
-                         int8_t* __restrict__ codes, double* __restrict__ scales) {
-  const int64_t row = blockIdx.x;
+                         int8_t* __restrict__ codes, double* __restrict__ scales, bool vec) {
+  const int64_t row = blockIdx.y;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kChunk;
   if (threadIdx.x == 0) pdl_launch_dependents();
   pdl_wait();
   const float a = amax[row];
   const double s = a == 0.0f ? 1.0 : static_cast<double>(a) / 127.0;  // quantize.cpp:120-125
   const double r = 1.0 / s;
-  if (threadIdx.x == 0) scales[row] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) scales[row] = s;
   const T* xr = x + row * k;
-  for (int64_t e = threadIdx.x; e < k; e += kThreads)
-    codes[row * k + e] = static_cast<int8_t>(quant_one(load1<T>(xr + e), s, r, -128, 127));
+  int8_t* cr = codes + row * k;
+  if (vec) {
+    for (int64_t e = c0 + threadIdx.x * 4; e < min(k, c0 + kChunk); e += kThreads * 4) {
+      float v[4];
+      load4<T>(xr + e, v);
+      char4 q;
+      q.x = static_cast<signed char>(quant_one(v[0], s, r, -128, 127));
+      q.y = static_cast<signed char>(quant_one(v[1], s, r, -128, 127));
+      q.z = static_cast<signed char>(quant_one(v[2], s, r, -128, 127));
+      q.w = static_cast<signed char>(quant_one(v[3], s, r, -128, 127));
+      *reinterpret_cast<char4*>(cr + e) = q;
+    }
+  } else {
+    for (int64_t e = c0 + threadIdx.x; e < min(k, c0 + kChunk); e += kThreads)
+      cr[e] = static_cast<int8_t>(quant_one(load1<T>(xr + e), s, r, -128, 127));
+  }
 }
 
 // out[i, j] = float((double(acc[i, j]) * 2^-e) * s_a[i])  (gemm.cpp:252, /2^e exact).
@@ -83,43 +116,66 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 template <typename K, typename... Args>
-void launch_pdl(K kern, dim3 grid, cudaStream_t s, Args... args) {
+void launch_opt(bool pdl, K kern, dim3 grid, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kThreads);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl && pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cuda_check(cudaLaunchKernelEx(&cfg, kern, args...), "tensor-parallel kernel launch");
   count_launch();
 }
 
+template <typename K, typename... Args>
+void launch_pdl(K kern, dim3 grid, cudaStream_t s, Args... args) {
+  launch_opt(true, kern, grid, s, args...);
+}
+
+
+}  // namespace
+
+namespace {
+dim3 chunk_grid(int64_t m, int64_t k) {
+  return dim3(static_cast<unsigned>(std::max<int64_t>(1, (k + kChunk - 1) / kChunk)),
+              static_cast<unsigned>(m));
+}
+bool vec_ok(const void* x, const void* codes, int64_t k, int elt) {
+  return k % 4 == 0 && reinterpret_cast<uintptr_t>(x) % (4 * elt) == 0 &&
+         (codes == nullptr || reinterpret_cast<uintptr_t>(codes) % 4 == 0);
+}
 }  // namespace
 
 void launch_row_absmax(const void* x, int x_dtype, int64_t m, int64_t k, float* amax,
                        cudaStream_t s) {
-  const dim3 grid(static_cast<unsigned>(m));
+  if (m <= 0) return;
+  cuda_check(cudaMemsetAsync(amax, 0, static_cast<size_t>(m) * sizeof(float), s), "memset(amax)");
+  const dim3 grid = chunk_grid(m, k);
+  // no programmatic overlap: the kernel's atomics must follow the memset
   if (x_dtype == ISB_F32)
-    launch_pdl(row_absmax_kernel<float>, grid, s, static_cast<const float*>(x), k, amax);
+    launch_opt(false, row_absmax_kernel<float>, grid, s, static_cast<const float*>(x), k, amax,
+               vec_ok(x, nullptr, k, 4));
   else if (x_dtype == ISB_BF16)
-    launch_pdl(row_absmax_kernel<__nv_bfloat16>, grid, s,
-               static_cast<const __nv_bfloat16*>(x), k, amax);
+    launch_opt(false, row_absmax_kernel<__nv_bfloat16>, grid, s,
+               static_cast<const __nv_bfloat16*>(x), k, amax, vec_ok(x, nullptr, k, 2));
   else
     fail(ISB_PARAM, "activation dtype must be float32 or bfloat16");
 }
 
 void launch_quantize_amax(const void* x, int x_dtype, int64_t m, int64_t k, const float* amax,
                           int8_t* codes, double* scales, cudaStream_t s) {
-  const dim3 grid(static_cast<unsigned>(m));
+  if (m <= 0) return;
+  const dim3 grid = chunk_grid(m, k);
   if (x_dtype == ISB_F32)
     launch_pdl(quantize_amax_kernel<float>, grid, s, static_cast<const float*>(x), k, amax,
-               codes, scales);
+               codes, scales, vec_ok(x, codes, k, 4));
   else if (x_dtype == ISB_BF16)
     launch_pdl(quantize_amax_kernel<__nv_bfloat16>, grid, s,
-               static_cast<const __nv_bfloat16*>(x), k, amax, codes, scales);
+               static_cast<const __nv_bfloat16*>(x), k, amax, codes, scales,
+               vec_ok(x, codes, k, 2));
   else
     fail(ISB_PARAM, "activation dtype must be float32 or bfloat16");
 }

@@ -59,14 +59,16 @@ def quantize_per_token(x: torch.Tensor, check_finite: bool = False, stream=None,
     return codes, scales
 
 
-def row_absmax(x: torch.Tensor, stream=None) -> torch.Tensor:
+def row_absmax(x: torch.Tensor, stream=None, out=None) -> torch.Tensor:
     """Per-row max|x| (float32 [M]) of a (local, K-sharded) activation slice — the
     partial a row-parallel layer all-reduces with MAX before quantizing."""
     x = _cuda(x)
     if x.dtype not in (torch.float32, torch.bfloat16) or x.dim() != 2:
         raise _lib.ParamError("activations must be 2-d float32 or bfloat16")
     m, k = x.shape
-    amax = torch.empty((m,), dtype=torch.float32, device=x.device)
+    amax = out if out is not None else torch.empty((m,), dtype=torch.float32, device=x.device)
+    if amax.dtype != torch.float32 or amax.numel() != m or not amax.is_contiguous():
+        raise _lib.ParamError("amax must be a contiguous float32 [M] tensor")
     check(load().isb_row_absmax(_ptr(x), _DT[x.dtype], m, k, _ptr(amax), _stream(stream)))
     return amax
 
