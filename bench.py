@@ -505,7 +505,9 @@ def run_ours(args, ws, rank, local):
     # Dominant kernel: the grouped layer launch (the whole step is this one kernel).
     achieved = layer_bytes / us_step / 1e3  # GB/s
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r02b_traffic.json")
+    if not os.path.exists(tpath):
+        tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(tpath) and m == 16:
         try:
             with open(tpath) as f:

@@ -186,22 +186,10 @@ bool pg_disabled() {
   return off;
 }
 
-// The stream-K decode kernel (gemm_decode.cu) is opt-in: ISB_DECODE=1. At the
-// LLaMA-2-7B decode shapes the cluster split-K kernel (gemm_tc.cu) is faster
-// (profiles/r01_decode_streamk.md); the stream-K kernel is kept for A/B work.
-bool decode_disabled() {
-  static const bool off = [] {
-    const char* e = std::getenv("ISB_DECODE");
-    return !(e && e[0] == '1');
-  }();
-  return off;
-}
-
 int64_t align256(int64_t b) { return (b + 255) / 256 * 256; }
 
 int64_t gemm_workspace_bytes(int64_t m, const isb_weight& w) {
   if (!w.tensor_core_ok()) return 0;
-  if (decode_eligible(m, w) && !decode_disabled()) return decode_workspace_bytes(m, w);
   return std::max(plan_gemm(m, w, num_sms(), ISB_PATH_INTEGER_SCALE).workspace_bytes,
                   plan_gemm(m, w, num_sms(), ISB_PATH_FLOAT_SCALE).workspace_bytes);
 }
@@ -250,13 +238,6 @@ void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
   if (path == ISB_PATH_INTEGER_SCALE) require_int32_safe(w);
   if (m > std::numeric_limits<int>::max() || w->n > std::numeric_limits<int>::max())
     fail(ISB_PARAM, "shape too large");
-  if (decode_eligible(m, *w) && !decode_disabled()) {
-    const int64_t need = decode_workspace_bytes(m, *w);
-    if (!ws || ws_bytes < need)
-      fail(ISB_PARAM, "workspace too small: need " + std::to_string(need) + " bytes");
-    launch_gemm_decode(path, xq, sa, m, *w, out, out_dtype, ws, num_sms(), as_stream(stream));
-    return;
-  }
   const GemmPlan pl = plan_gemm(m, *w, num_sms(), path);
   if (!ws || ws_bytes < pl.workspace_bytes)
     fail(ISB_PARAM, "workspace too small: need " + std::to_string(pl.workspace_bytes) + " bytes");

@@ -11,19 +11,22 @@
 // bit-identical to the per-group kernel: every partial sum is bounded by the
 // static overflow bound (analysis.cpp:24-59), which callers gate on.
 //
-// Tile: 128 output channels (UMMA M) x 192 tokens (UMMA N), persistent CTAs.
-// TMEM: A ring 4 x 32 columns (expanded weights) + 2 x 192-column int32
-// accumulators, so the epilogue of tile t overlaps the MMAs of tile t+1.
+// Used for 256 <= M < 512 (M >= 512 runs the CTA-pair kernel, gemm_sp.cu). Tile: 128
+// output channels (UMMA M) x 256 tokens (UMMA N), persistent 1-CTA tiles, both MMA
+// operands in shared memory (SS form): two transform warpgroups write the folded weights
+// into a 2-slot SWIZZLE_128B ring, activations arrive by TMA into a 4-stage ring recycled
+// by the MMA, packed weights + k_g by bulk copy into a 6-slot ring; TMEM holds 2 x 256
+// int32 accumulator columns so the epilogue of tile t overlaps the MMAs of tile t+1.
 //
-//   warp 0      producer : per 128-K block one bulk copy of the 8 KiB packed
-//                          weight block + 512 B of k_g, and a TMA (SWIZZLE_128B)
-//                          of the 192 x 128 int8 activation tile.
+//   warp 0      producer : packed weights + k_g (bulk copies).
+//   warp 3      producer : activation tiles (TMA, SWIZZLE_128B).
 //   warp 1      MMA      : 4 x tcgen05.mma.kind::i8 (K = 32) per block into D[t & 1].
 //   warp 2      TMEM allocator.
 //   warps 4-11  transform: two warpgroups alternate blocks; thread r owns channel r:
 //                          nibble -> fp16 lane (exponent-bias trick) -> one HFMA2
-//                          computes 1536 + k*c exactly -> low byte = k*c.
-//   warps 12-15 epilogue : tcgen05.ld of D, out = float((double(acc) / 2^e) * s_a).
+//                          computes 1536 + k*c exactly -> low byte = k*c (fold.cuh).
+//   warps 12-27 epilogue : four warpgroups, 64 tokens each: tcgen05.ld of D,
+//                          out = float((double)acc * (s_a * 2^-e)).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -42,16 +45,7 @@
 namespace isb {
 namespace {
 
-constexpr int kFMT = 192;                     // tokens per tile (UMMA N)
-constexpr int kFXBytes = kFMT * 128;          // 24 KiB activation tile per block
-constexpr int kFStage = kBlockBytes + kFXBytes;  // 32 KiB (W first, X 1024-aligned)
-constexpr int kFNA = 4;                       // TMEM A ring
 constexpr int kFXformWG = 2;
-constexpr int kFThreads = 128 + 128 * kFXformWG + 128;
-constexpr int kFStages = 6;
-constexpr int kFSmem = 1024 + kFStages * (kFStage + kTileN * 4) + 2 * kFMT * 8 + 512;
-static_assert(kFSmem <= 227 * 1024, "smem");
-constexpr uint32_t kFDCol = kFNA * 32;        // D buffers start after the A ring
 
 struct FoldParams {
   const uint8_t* packed;  // [n_tiles][kblocks][8 KiB]
@@ -71,223 +65,6 @@ __device__ __forceinline__ void store_out_f(void* out, int dtype, int64_t idx, f
   else
     static_cast<__half*>(out)[idx] = __float2half_rn(f);
 }
-
-__global__ void __launch_bounds__(kFThreads, 1)
-    gemm_w4a8_fold(const __grid_constant__ CUtensorMap x_map, const FoldParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* smem_sc = smem + kFStages * kFStage;                        // [stage][128] k_g
-  double* sa_s = reinterpret_cast<double*>(smem_sc + kFStages * kTileN * 4);  // [2][MT]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sa_s + 2 * kFMT);
-  uint64_t* empty = full + kFStages;
-  uint64_t* a_full = empty + kFStages;
-  uint64_t* a_empty = a_full + kFNA;
-  uint64_t* d_full = a_empty + kFNA;
-  uint64_t* d_empty = d_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
-
-  const uint32_t warp = warp_id();
-  const uint32_t lane = lane_id();
-  const int ntiles = static_cast<int>(blockIdx.x) < p.tiles
-                         ? (p.tiles - static_cast<int>(blockIdx.x) + gridDim.x - 1) / gridDim.x
-                         : 0;
-  const int total = ntiles * p.kblocks;  // (tile, block) steps of this CTA
-
-  if (warp == 0 && lane == 0) {
-    prefetch_tensormap(&x_map);
-    for (int i = 0; i < kFStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1 + 4);
-    }
-    for (int i = 0; i < kFNA; ++i) {
-      mbar_init(&a_full[i], 4);
-      mbar_init(&a_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&d_full[i], 1);
-      mbar_init(&d_empty[i], 4);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) pdl_launch_dependents();
-
-  auto tile_of = [&](int it, int& nt, int& mt) {
-    const int t = blockIdx.x + it * gridDim.x;
-    nt = t / p.m_tiles;
-    mt = t % p.m_tiles;
-  };
-
-  if (warp == 0) {
-    // ---------------------------------------------------------------- producer
-    if (elect_one()) {
-      auto load_static = [&](int j, int stage) {
-        int nt, mt;
-        tile_of(j / p.kblocks, nt, mt);
-        const int kb = j % p.kblocks;
-        mbar_arrive_expect_tx(&full[stage], kFStage + kTileN * 4);
-        bulk_load(smem + stage * kFStage,
-                  p.packed + (static_cast<int64_t>(nt) * p.kblocks + kb) * kBlockBytes,
-                  kBlockBytes, &full[stage]);
-        bulk_load(smem_sc + stage * kTileN * 4,
-                  p.kscale + (static_cast<int64_t>(nt) * p.G + kb / p.gb) * kTileN, kTileN * 4,
-                  &full[stage]);
-      };
-      const int pre = min(total, kFStages);
-      for (int j = 0; j < pre; ++j) load_static(j, j);
-      pdl_wait();
-      for (int j = 0; j < total; ++j) {
-        const int stage = j % kFStages;
-        if (j >= pre) {
-          mbar_wait(&empty[stage], ((j / kFStages) & 1) ^ 1);
-          load_static(j, stage);
-        }
-        int nt, mt;
-        tile_of(j / p.kblocks, nt, mt);
-        tma_load_2d(smem + stage * kFStage + kBlockBytes, &x_map, &full[stage],
-                    (j % p.kblocks) * kBlockK, mt * kFMT);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    // ---------------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc = make_idesc_i8(128, kFMT);
-    const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
-    const uint32_t s_base = smem_u32(smem);
-    int j = 0;
-    for (int it = 0; it < ntiles; ++it) {
-      const int ds = it & 1;
-      mbar_wait(&d_empty[ds], ((it >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tbase + kFDCol + ds * kFMT;
-      for (int kb = 0; kb < p.kblocks; ++kb, ++j) {
-        const int stage = j % kFStages, as = j % kFNA;
-        mbar_wait(&a_full[as], (j / kFNA) & 1);  // implies full[stage] (transform saw it)
-        tc_fence_after();
-        const uint64_t bdesc = make_sw128_kmajor_desc(s_base + stage * kFStage + kBlockBytes);
-        const uint32_t a_tmem = tbase + as * 32;
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          mma_i8_ts_warp(d_tmem, a_tmem + c * 8, bdesc + static_cast<uint64_t>(c * 2), idesc,
-                         (kb > 0 || c > 0) ? 1u : 0u);
-        mma_commit_warp(&empty[stage]);
-        mma_commit_warp(&a_empty[as]);
-      }
-      mma_commit_warp(&d_full[ds]);
-    }
-  } else if (warp >= 4 && warp < 4 + 4 * kFXformWG) {
-    // ---------------------------------------------------------------- transform
-    const int xw = static_cast<int>(warp - 4) / 4;
-    const uint32_t r = (warp % 4) * 32 + lane;  // output channel == TMEM lane
-    const uint32_t lane_base = ((warp % 4) * 32) << 16;
-    const uint32_t w_base = smem_u32(smem) + r * 16;
-    const uint32_t sc_base = smem_u32(smem_sc) + r * 4;
-    for (int j = xw; j < total; j += kFXformWG) {
-      const int stage = j % kFStages, as = j % kFNA;
-      mbar_wait(&full[stage], (j / kFStages) & 1);
-      uint4 q[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) q[c] = ld_shared_v4(w_base + stage * kFStage + c * (kTileN * 16));
-      const int32_t k = static_cast<int32_t>(ld_shared_u32(sc_base + stage * kTileN * 4));
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the async refill
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      const float kf = static_cast<float>(k);
-      const uint32_t k1 = half2_bits(kf);
-      const uint32_t k16 = half2_bits(kf * 0.0625f);
-      const uint32_t cA = half2_bits(1536.0f - 1032.0f * kf);
-      const uint32_t cB = half2_bits(1536.0f - 72.0f * kf);
-      uint32_t a[32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t w4[4] = {q[c].x, q[c].y, q[c].z, q[c].w};
-#pragma unroll
-        for (int w = 0; w < 4; ++w) fold_word(w4[w], k1, k16, cA, cB, a[c * 8 + 2 * w], a[c * 8 + 2 * w + 1]);
-      }
-      mbar_wait(&a_empty[as], ((j / kFNA) & 1) ^ 1);
-      tc_fence_after();
-      tmem_st_x32(tmem_base + lane_base + as * 32, a);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a_full[as]);
-    }
-  } else if (warp >= 4 + 4 * kFXformWG) {
-    // ---------------------------------------------------------------- epilogue
-    const uint32_t ew = warp - (4 + 4 * kFXformWG);
-    const uint32_t t128 = ew * 32 + lane;
-    const uint32_t r = t128;                      // TMEM lane == channel in tile
-    const uint32_t lane_base = (ew * 32) << 16;
-    pdl_wait();  // sa / out may be touched by the preceding grid
-    auto sa_prefetch = [&](int it) {
-      if (it < ntiles) {
-        int nt, mt;
-        tile_of(it, nt, mt);
-        for (int t = t128; t < kFMT; t += 128) {
-          const int64_t m = static_cast<int64_t>(mt) * kFMT + t;
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
-                           smem_u32(sa_s + (it & 1) * kFMT + t)),
-                       "l"(p.sa + (m < p.M ? m : 0)), "r"(m < p.M ? 8 : 0)
-                       : "memory");
-        }
-      }
-      cp_async_commit();
-    };
-    sa_prefetch(0);
-    for (int it = 0; it < ntiles; ++it) {
-      int nt, mt;
-      tile_of(it, nt, mt);
-      const int ds = it & 1;
-      sa_prefetch(it + 1);
-      cp_async_wait<1>();
-      named_bar_sync(1, 128);  // sa_s[it & 1] complete for all epilogue threads
-      const double* sa_t = sa_s + (it & 1) * kFMT;
-      mbar_wait(&d_full[ds], (it >> 1) & 1);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + lane_base + kFDCol + ds * kFMT;
-      const int64_t n = static_cast<int64_t>(nt) * kTileN + r;
-      const int64_t m0 = static_cast<int64_t>(mt) * kFMT;
-#pragma unroll 1
-      for (int cc = 0; cc < kFMT; cc += 32) {
-        uint32_t v[32];
-        tmem_ld_x16_(taddr + cc, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
-        tmem_ld_x16_(taddr + cc + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
-        tmem_wait_ld();
-        if (cc + 32 >= kFMT) {  // all of D[ds] read: hand it back to the MMA warp
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&d_empty[ds]);
-        }
-        if (n < p.N) {
-#pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const int64_t m = m0 + cc + t;
-            if (m < p.M) {
-              if (p.out_dtype == ISB_I32) {  // raw acc (row-parallel TP)
-                static_cast<int32_t*>(p.out)[m * p.N + n] = static_cast<int32_t>(v[t]);
-              } else {
-                const double o = __dmul_rn(
-                    static_cast<double>(static_cast<int32_t>(v[t])) * p.inv_amp, sa_t[cc + t]);
-                store_out_f(p.out, p.out_dtype, m * p.N + n, __double2float_rn(o));
-              }
-            }
-          }
-        }
-      }
-      named_bar_sync(1, 128);  // done with sa_s[it & 1] before it is refilled
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) tmem_dealloc(tmem_base, 512);
-}
-
 
 // ============================================================================
 // SS variant: the transform warps write the folded int8 weights into a shared-
@@ -662,359 +439,6 @@ void launch_fold_ss(const int8_t* xq, int64_t m, const isb_weight& w, FoldParams
   count_launch();
 }
 
-// ============================================================================
-// 2-SM variant (tcgen05.mma.cta_group::2). A CTA pair computes 256 channels
-// (each CTA its own 128: weights expanded into its own TMEM) x 192 tokens; each
-// CTA TMA-loads only HALF of the activation tile (96 tokens) into its own smem
-// and the pair's MMA reads both halves. Per SM and 128-K block that is 8 KiB of
-// weights + 12 KiB of activations for 3.1 M MACs — 151 MAC/B instead of 96,
-// aimed at the per-SM L2->SMEM ingest bound of the 1-SM kernel. The leader
-// (cluster rank 0) issues the MMAs; commits are multicast to both CTAs; the
-// peer's transform and epilogue arrive on the leader's barriers over DSMEM.
-constexpr int k2MT = 192;                        // tokens per pair tile (UMMA N)
-constexpr int k2XH = (k2MT / 2) * 128;           // 12 KiB activation half per CTA
-constexpr int k2Stage = kBlockBytes + k2XH;      // [W 8 KiB][X half 12 KiB]
-constexpr int k2Stages = 8;
-constexpr int k2NA = 4;
-constexpr int k2Threads = 128 + 128 * 2 + 128;
-constexpr int k2Smem = 1024 + k2Stages * (k2Stage + kTileN * 4) + 2 * k2MT * 8 + 512;
-static_assert(k2Smem <= 227 * 1024, "smem");
-static_assert(k2Stage % 1024 == 0, "SW128 activation tiles need 1 KiB alignment");
-constexpr uint32_t k2DCol = k2NA * 32;
-static_assert(k2DCol + 2 * k2MT <= 512, "TMEM");
-
-struct Fold2Params {
-  const uint8_t* packed;
-  const int32_t* kscale;
-  const double* sa;
-  void* out;
-  int M, N, G, gb, kblocks, m_tiles, n_tiles, units, out_dtype;
-  double inv_amp;
-};
-
-__device__ __forceinline__ void arrive_on_leader(uint64_t* bar, uint32_t rank) {
-  if (rank == 0)
-    mbar_arrive(bar);
-  else
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                     mapa_shared(smem_u32(bar), 0))
-                 : "memory");
-}
-
-__device__ __forceinline__ void mma_i8_ts_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                              uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(
-          d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u)
-      : "memory");
-}
-
-__device__ __forceinline__ void commit_2sm_mc(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
-          smem_u32(bar)),
-      "h"(static_cast<uint16_t>(3))
-      : "memory");
-}
-
-__global__ void __launch_bounds__(k2Threads, 1)
-    gemm_w4a8_fold2(const __grid_constant__ CUtensorMap x_map, const Fold2Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* smem_sc = smem + k2Stages * k2Stage;                          // [stage][128] k_g
-  double* sa_s = reinterpret_cast<double*>(smem_sc + k2Stages * kTileN * 4);  // [2][MT]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sa_s + 2 * k2MT);    // local: W + k_g
-  uint64_t* xfull = full + k2Stages;        // leader: both activation halves
-  uint64_t* empty = xfull + k2Stages;       // local: transform (W) + MMA commit (X)
-  uint64_t* a_full = empty + k2Stages;      // leader: both CTAs' expanded weights
-  uint64_t* a_empty = a_full + k2NA;        // local (multicast commit)
-  uint64_t* d_full = a_empty + k2NA;        // local (multicast commit)
-  uint64_t* d_empty = d_full + 2;           // leader: both CTAs drained D
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
-
-  const uint32_t warp = warp_id();
-  const uint32_t lane = lane_id();
-  const uint32_t rank = cluster_ctarank();
-  const int cid = static_cast<int>(blockIdx.x) / 2, ncl = static_cast<int>(gridDim.x) / 2;
-  const int nunits = cid < p.units ? (p.units - cid + ncl - 1) / ncl : 0;
-  const int total = nunits * p.kblocks;
-
-  if (warp == 0 && lane == 0) {
-    prefetch_tensormap(&x_map);
-    for (int i = 0; i < k2Stages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&xfull[i], 1);
-      mbar_init(&empty[i], 1 + 4);
-    }
-    for (int i = 0; i < k2NA; ++i) {
-      mbar_init(&a_full[i], 8);
-      mbar_init(&a_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&d_full[i], 1);
-      mbar_init(&d_empty[i], 8);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) pdl_launch_dependents();
-
-  auto unit_of = [&](int it, int& np, int& mt) {
-    const int u = cid + it * ncl;
-    np = u / p.m_tiles;
-    mt = u % p.m_tiles;
-  };
-
-  if (warp == 0) {
-    // ---------------------------------------------------------------- producer
-    if (lane == 0) {
-      const uint32_t xfull_leader = mapa_shared(smem_u32(xfull), 0);
-      auto load_static = [&](int j, int stage) {
-        int np, mt;
-        unit_of(j / p.kblocks, np, mt);
-        const int kb = j % p.kblocks;
-        const int nt = np * 2 + static_cast<int>(rank);
-        if (nt < p.n_tiles) {
-          mbar_arrive_expect_tx(&full[stage], kBlockBytes + kTileN * 4);
-          bulk_load(smem + stage * k2Stage,
-                    p.packed + (static_cast<int64_t>(nt) * p.kblocks + kb) * kBlockBytes,
-                    kBlockBytes, &full[stage]);
-          bulk_load(smem_sc + stage * kTileN * 4,
-                    p.kscale + (static_cast<int64_t>(nt) * p.G + kb / p.gb) * kTileN,
-                    kTileN * 4, &full[stage]);
-        } else {
-          mbar_arrive(&full[stage]);  // no channels here: the transform writes zeros
-        }
-      };
-      auto load_x = [&](int j, int stage) {
-        int np, mt;
-        unit_of(j / p.kblocks, np, mt);
-        if (rank == 0) mbar_arrive_expect_tx(&xfull[stage], 2 * k2XH);  // both halves
-        asm volatile(
-            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem + stage * k2Stage + kBlockBytes)),
-            "l"(reinterpret_cast<uint64_t>(&x_map)),
-            "r"(xfull_leader + static_cast<uint32_t>(stage) * 8u),
-            "r"((j % p.kblocks) * kBlockK), "r"(mt * k2MT + static_cast<int>(rank) * (k2MT / 2))
-            : "memory");
-      };
-      const int pre = min(total, k2Stages);
-      for (int j = 0; j < pre; ++j) load_static(j, j);
-      pdl_wait();
-      for (int j = 0; j < total; ++j) {
-        const int stage = j % k2Stages;
-        if (j >= pre) {
-          mbar_wait(&empty[stage], ((j / k2Stages) & 1) ^ 1);
-          load_static(j, stage);
-        }
-        load_x(j, stage);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    // ---------------------------------------------------------------- MMA issuer (leader)
-    if (rank == 0) {
-      constexpr uint32_t idesc = make_idesc_i8(256, k2MT);
-      const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
-      const uint32_t s_base = smem_u32(smem);
-      int j = 0;
-      for (int it = 0; it < nunits; ++it) {
-        const int ds = it & 1;
-        mbar_wait(&d_empty[ds], ((it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tbase + k2DCol + ds * k2MT;
-        for (int kb = 0; kb < p.kblocks; ++kb, ++j) {
-          const int stage = j % k2Stages, as = j % k2NA;
-          mbar_wait(&xfull[stage], (j / k2Stages) & 1);
-          mbar_wait(&a_full[as], (j / k2NA) & 1);
-          tc_fence_after();
-          const uint64_t bdesc = make_sw128_kmajor_desc(s_base + stage * k2Stage + kBlockBytes);
-          const uint32_t a_tmem = tbase + as * 32;
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            mma_i8_ts_2sm(d_tmem, a_tmem + c * 8, bdesc + static_cast<uint64_t>(c * 2), idesc,
-                          (kb > 0 || c > 0) ? 1u : 0u);
-          commit_2sm_mc(&empty[stage]);
-          commit_2sm_mc(&a_empty[as]);
-        }
-        commit_2sm_mc(&d_full[ds]);
-      }
-    }
-  } else if (warp >= 4 && warp < 12) {
-    // ---------------------------------------------------------------- transform
-    const int xw = static_cast<int>(warp - 4) / 4;
-    const uint32_t r = (warp % 4) * 32 + lane;
-    const uint32_t lane_base = ((warp % 4) * 32) << 16;
-    const uint32_t w_base = smem_u32(smem) + r * 16;
-    const uint32_t sc_base = smem_u32(smem_sc) + r * 4;
-    for (int j = xw; j < total; j += 2) {
-      const int stage = j % k2Stages, as = j % k2NA;
-      int np, mt;
-      unit_of(j / p.kblocks, np, mt);
-      const bool valid = np * 2 + static_cast<int>(rank) < p.n_tiles;
-      mbar_wait(&full[stage], (j / k2Stages) & 1);
-      uint4 q[4];
-      int32_t k = 0;
-      if (valid) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) q[c] = ld_shared_v4(w_base + stage * k2Stage + c * (kTileN * 16));
-        k = static_cast<int32_t>(ld_shared_u32(sc_base + stage * kTileN * 4));
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the async refill
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      uint32_t a[32];
-      if (valid) {
-        const float kf = static_cast<float>(k);
-        const uint32_t k1 = half2_bits(kf);
-        const uint32_t k16 = half2_bits(kf * 0.0625f);
-        const uint32_t cA = half2_bits(1536.0f - 1032.0f * kf);
-        const uint32_t cB = half2_bits(1536.0f - 72.0f * kf);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint32_t w4[4] = {q[c].x, q[c].y, q[c].z, q[c].w};
-#pragma unroll
-          for (int w = 0; w < 4; ++w)
-            fold_word(w4[w], k1, k16, cA, cB, a[c * 8 + 2 * w], a[c * 8 + 2 * w + 1]);
-        }
-      } else {
-#pragma unroll
-        for (int z = 0; z < 32; ++z) a[z] = 0u;
-      }
-      mbar_wait(&a_empty[as], ((j / k2NA) & 1) ^ 1);
-      tc_fence_after();
-      tmem_st_x32(tmem_base + lane_base + as * 32, a);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) arrive_on_leader(&a_full[as], rank);
-    }
-  } else if (warp >= 12) {
-    // ---------------------------------------------------------------- epilogue
-    const uint32_t ew = warp - 12;
-    const uint32_t t128 = ew * 32 + lane;
-    const uint32_t r = t128;
-    const uint32_t lane_base = (ew * 32) << 16;
-    pdl_wait();
-    auto sa_prefetch = [&](int it) {
-      if (it < nunits) {
-        int np, mt;
-        unit_of(it, np, mt);
-        for (int t = t128; t < k2MT; t += 128) {
-          const int64_t m = static_cast<int64_t>(mt) * k2MT + t;
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
-                           smem_u32(sa_s + (it & 1) * k2MT + t)),
-                       "l"(p.sa + (m < p.M ? m : 0)), "r"(m < p.M ? 8 : 0)
-                       : "memory");
-        }
-      }
-      cp_async_commit();
-    };
-    sa_prefetch(0);
-    for (int it = 0; it < nunits; ++it) {
-      int np, mt;
-      unit_of(it, np, mt);
-      const int ds = it & 1;
-      sa_prefetch(it + 1);
-      cp_async_wait<1>();
-      named_bar_sync(1, 128);
-      const double* sa_t = sa_s + (it & 1) * k2MT;
-      mbar_wait(&d_full[ds], (it >> 1) & 1);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + lane_base + k2DCol + ds * k2MT;
-      const int64_t n = static_cast<int64_t>(np * 2 + static_cast<int>(rank)) * kTileN + r;
-      const int64_t m0 = static_cast<int64_t>(mt) * k2MT;
-#pragma unroll 1
-      for (int cc = 0; cc < k2MT; cc += 32) {
-        uint32_t v[32];
-        tmem_ld_x16_(taddr + cc, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
-        tmem_ld_x16_(taddr + cc + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
-        tmem_wait_ld();
-        if (cc + 32 >= k2MT) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) arrive_on_leader(&d_empty[ds], rank);
-        }
-        if (n < p.N) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int64_t m = m0 + cc + i;
-            if (m < p.M) {
-              if (p.out_dtype == ISB_I32) {
-                static_cast<int32_t*>(p.out)[m * p.N + n] = static_cast<int32_t>(v[i]);
-              } else {
-                const double o = __dmul_rn(
-                    static_cast<double>(static_cast<int32_t>(v[i])) * p.inv_amp, sa_t[cc + i]);
-                store_out_f(p.out, p.out_dtype, m * p.N + n, __double2float_rn(o));
-              }
-            }
-          }
-        }
-      }
-      named_bar_sync(1, 128);
-    }
-  }
-
-  tc_fence_before();
-  cluster_sync_all();  // no peer arrives on our barriers after this point
-  if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(512)
-                 : "memory");
-}
-
-// Opt-in (ISB_FOLD2=1): bit-exact, but measured slower than the 1-SM kernel at the
-// LLaMA-2-7B prefill shapes (1040 vs 1422 TOPS at M = 2048).
-bool fold2_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("ISB_FOLD2");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
-void launch_fold2(const CUtensorMap& map, const Fold2Params& prm, int num_sms, cudaStream_t s) {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(gemm_w4a8_fold2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    k2Smem),
-               "cudaFuncSetAttribute(fold2 smem)");
-  });
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * std::min(prm.units, num_sms / 2));
-  cfg.blockDim = dim3(k2Threads);
-  cfg.dynamicSmemBytes = k2Smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = 2;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  cuda_check(cudaLaunchKernelEx(&cfg, gemm_w4a8_fold2, map, prm), "gemm_w4a8_fold2 launch");
-  count_launch();
-}
-
 }  // namespace
 
 bool fold_eligible(int64_t m, const isb_weight& w, int path) {
@@ -1024,12 +448,6 @@ bool fold_eligible(int64_t m, const isb_weight& w, int path) {
 
 void launch_gemm_fold(const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                       void* out, int out_dtype, int num_sms, cudaStream_t s) {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(gemm_w4a8_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kFSmem),
-               "cudaFuncSetAttribute(fold smem)");
-  });
   FoldParams prm{};
   prm.packed = w.packed;
   prm.kscale = w.kscale_tiled;
@@ -1040,56 +458,10 @@ void launch_gemm_fold(const int8_t* xq, const double* sa, int64_t m, const isb_w
   prm.G = static_cast<int>(w.groups);
   prm.gb = static_cast<int>(w.group / kBlockK);
   prm.kblocks = static_cast<int>(w.kblocks);
-  prm.m_tiles = static_cast<int>((m + kFMT - 1) / kFMT);
-  prm.tiles = static_cast<int>(w.n_tiles) * prm.m_tiles;
   prm.out_dtype = out_dtype;
   prm.inv_amp = std::ldexp(1.0, -w.exponent);
   prm.dbg = g_dbg;
-  if (fold2_enabled()) {
-    Fold2Params p2{};
-    p2.packed = w.packed;
-    p2.kscale = w.kscale_tiled;
-    p2.sa = sa;
-    p2.out = out;
-    p2.M = static_cast<int>(m);
-    p2.N = static_cast<int>(w.n);
-    p2.G = static_cast<int>(w.groups);
-    p2.gb = static_cast<int>(w.group / kBlockK);
-    p2.kblocks = static_cast<int>(w.kblocks);
-    p2.m_tiles = static_cast<int>((m + k2MT - 1) / k2MT);
-    p2.n_tiles = static_cast<int>(w.n_tiles);
-    p2.units = static_cast<int>((w.n_tiles + 1) / 2) * p2.m_tiles;
-    p2.out_dtype = out_dtype;
-    p2.inv_amp = std::ldexp(1.0, -w.exponent);
-    launch_fold2(make_x_map(xq, m, w.k, k2MT / 2), p2, num_sms, s);
-    return;
-  }
-  static const int ss_mt = [] {  // default: SS kernel, 256-token tiles; ISB_FOLD_SS=0: TS kernel
-    const char* e = std::getenv("ISB_FOLD_SS");
-    return e ? std::atoi(e) : 256;
-  }();
-  if (ss_mt == 256) {  // four epilogue warpgroups (64 tokens each)
-    launch_fold_ss<256, 2, 4, 6, 4>(xq, m, w, prm, num_sms, s);
-    return;
-  }
-  if (ss_mt == 2562) {  // two epilogue warpgroups
-    launch_fold_ss<256, 2, 4, 6, 2>(xq, m, w, prm, num_sms, s);
-    return;
-  }
-
-  const CUtensorMap map = make_x_map(xq, m, w.k, kFMT);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(std::min(prm.tiles, num_sms));
-  cfg.blockDim = dim3(kFThreads);
-  cfg.dynamicSmemBytes = kFSmem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cuda_check(cudaLaunchKernelEx(&cfg, gemm_w4a8_fold, map, prm), "gemm_w4a8_fold launch");
-  count_launch();
+  launch_fold_ss<256, 2, 4, 6, 4>(xq, m, w, prm, num_sms, s);  // four epilogue warpgroups
 }
 
 }  // namespace isb

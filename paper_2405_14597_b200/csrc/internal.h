@@ -105,13 +105,6 @@ constexpr int64_t kPgMinM = 128;
 bool pg_eligible(int64_t m, const isb_weight& w);
 void launch_gemm_pg(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
                     void* out, int out_dtype, int num_sms, cudaStream_t s);
-// Decode K3d/K4d (gemm_decode.cu): stream-K over all SMs, two CTAs per SM.
-constexpr int64_t kDecodeMaxM = 32;
-bool decode_eligible(int64_t m, const isb_weight& w);
-int64_t decode_workspace_bytes(int64_t m, const isb_weight& w);
-void launch_gemm_decode(int path, const int8_t* xq, const double* sa, int64_t m,
-                        const isb_weight& w, void* out, int out_dtype, void* workspace,
-                        int num_sms, cudaStream_t s);
 // Dense fp16/bf16 baseline (gemm_f16.cu): out = x[M][K] * w[N][K]^T, K % 64 == 0.
 void launch_gemm_dense(const void* x, const void* w, int64_t m, int64_t n, int64_t k, void* out,
                        int out_dtype, bool bf16, int num_sms, cudaStream_t s);

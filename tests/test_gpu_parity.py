@@ -190,45 +190,12 @@ def test_workspace_is_left_clean_and_results_repeat():
     assert int(ws.buf.view(torch.int32).abs().sum()) == 0  # split-K workspace left clean
 
 
-@pytest.mark.parametrize("env_kv", [("ISB_FOLD2", "1"), ("ISB_FOLD_SS", "0")],
-                         ids=["cta_group2", "tmem_operand"])
-def test_fold_variant_kernels_subprocess(env_kv):
-    """The opt-in prefill kernels — cta_group::2 pairs (ISB_FOLD2=1) and the TMEM-operand
-    (TS) kernel (ISB_FOLD_SS=0) — bit-exact on the fold tests (read once per process)."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, **{env_kv[0]: env_kv[1]})
-    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
-                        os.path.join(root, "tests", "test_gpu_parity.py"),
-                        "-k", "fold and not subprocess"],
-                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-
-
-def test_decode_stream_k_kernel_subprocess():
-    """The opt-in stream-K decode kernel (ISB_DECODE=1, read once per process):
-    bit-exact int32 / float32 on every split pattern, workspace left clean."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, ISB_DECODE="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
-                        os.path.join(root, "tests", "test_gpu_parity.py"),
-                        "-k", "test_decode_stream_k_bit_exact or workspace_is_left_clean"],
-                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-
-
 @pytest.mark.parametrize("m", [1, 5, 16, 17, 32])
 @pytest.mark.parametrize("k,n,g", [(4096, 12288, 128), (11008, 4096, 128), (4096, 22016, 128),
                                    (11008, 1000, 256), (2048, 640, 512), (256, 4, 128)])
 def test_decode_stream_k_bit_exact(m, k, n, g):
     """Decode shapes on every LLaMA-2-7B linear plus ragged N / g > 128: int32 acc
-    and float32 output bit-exact for every split pattern (default cluster kernel;
-    the stream-K kernel when run under ISB_DECODE=1)."""
+    and float32 output bit-exact for every split pattern of the cluster split-K kernel."""
     x, w, s, _, _ = llama_problem(m, k, n, seed_w=7 + n + g, seed_x=11 + m, g=g)
     ref = O.gemm_integer_scale(x, w, s)
     pw = pack(w, s)
