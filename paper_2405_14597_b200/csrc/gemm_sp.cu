@@ -91,11 +91,13 @@ __device__ __forceinline__ void sp_trace(const SpParams& p, int row, int idx) {
     p.trace[(row + 16 * static_cast<int>(blockIdx.x)) * 512 + idx] = clock64_();
 }
 
-template <int SX, int NXW, int EW>
+template <int SX, int NXW, int EW, int WPB>
 struct SpCfg {
+  static constexpr int kXW = NXW * WPB;  // transform warps: WPB per block slot
   static constexpr int kEW = EW;  // epilogue warpgroups: EW / 2 per token sub-tile
-  static constexpr int kThreads = 128 + 32 * NXW + 128 * kEW;
-  static constexpr int kStage = 32 * 64;  // per epilogue warp: 32 tokens x 32 channels of bf16
+  static constexpr int kThreads = 128 + 32 * kXW + 128 * kEW;
+  static constexpr int kStageTok = 16;                // tokens per staging round
+  static constexpr int kStage = kStageTok * 64;       // per epilogue warp: 16 tokens x 32 bf16 channels
   static constexpr int kSmem = 1024 + SX * kSpXStage + NXW * (kSpBBytes + kSpWBytes + kSpSc) +
                                4 * EW * kStage + 1024;
   static_assert(kSmem <= 227 * 1024, "smem");
@@ -184,10 +186,10 @@ __device__ __forceinline__ float eq2_fast(int32_t acc, float2 s, bool& slow) {
   return f;
 }
 
-template <int SX, int NXW, int EW>
-__global__ void __launch_bounds__(SpCfg<SX, NXW, EW>::kThreads, 1)
+template <int SX, int NXW, int EW, int WPB>
+__global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB>::kThreads, 1)
     gemm_w4a8_sp(const __grid_constant__ SpMaps maps, const __grid_constant__ SpParams p) {
-  using C = SpCfg<SX, NXW, EW>;
+  using C = SpCfg<SX, NXW, EW, WPB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -236,8 +238,8 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW>::kThreads, 1)
     for (int i = 0; i < p.nprob; ++i) prefetch_tensormap(&maps.x[i]);
     for (int i = 0; i < NXW; ++i) {
       mbar_init(&wfull[i], 1);
-      mbar_init(&wempty[i], 1);
-      mbar_init(&bfull[i], 2);
+      mbar_init(&wempty[i], WPB);
+      mbar_init(&bfull[i], 2 * WPB);
       mbar_init(&bempty[i], 1);
     }
     for (int i = 0; i < SX; ++i) {
@@ -351,9 +353,10 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW>::kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= 4 && warp < 4 + NXW) {
+  } else if (warp >= 4 && warp < 4 + C::kXW) {
     // ------------------------------------------------ transform: one warp per block
-    const int xw = static_cast<int>(warp) - 4;
+    const int xw = (static_cast<int>(warp) - 4) / WPB;     // block slot
+    const int half = (static_cast<int>(warp) - 4) % WPB;   // which rows of the slot (WPB = 2)
     int total = 0;
     for (int it = 0; it < nunits; ++it) {
       int pb, nt, mt;
@@ -367,8 +370,8 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW>::kThreads, 1)
       swait(&wfull[xw], u & 1, p.dbg);
       swait(&bempty[xw], (u & 1) ^ 1, p.dbg);
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const uint32_t row = lane + 32 * i;  // channel row within this CTA's 64
+      for (int i = 0; i < 2 / WPB; ++i) {
+        const uint32_t row = lane + 32 * (WPB == 1 ? i : half);  // channel row of this CTA's 64
         uint4 w4[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) w4[c] = ld_shared_v4(w_slot + c * (kSpWBytes / 4) + row * 16);
@@ -402,12 +405,12 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW>::kThreads, 1)
       if (lane == 0) {
         mbar_arrive(&wempty[xw]);
         arrive_leader(&bfull[xw], rank);
-        if (xw == 0) sp_trace(p, 5, u);
+        if (xw == 0 && half == 0) sp_trace(p, 5, u);
       }
     }
-  } else if (warp >= 4 + NXW) {
+  } else if (warp >= 4 + C::kXW) {
     // ------------------------------------------------ epilogue
-    const uint32_t ew = warp - (4 + NXW);
+    const uint32_t ew = warp - (4 + C::kXW);
     constexpr int kWgPerSub = EW / 2;             // warpgroups sharing one sub-tile
     constexpr int kChunks = 4 / kWgPerSub;        // 32-channel chunks per warpgroup
     const int sub = static_cast<int>(ew / 4) / kWgPerSub;
@@ -531,22 +534,31 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW>::kThreads, 1)
           // pieces): lane l writes token l's four 16-byte quads (rotated by l/2: bank-
           // conflict-free), then reads quad l%4 of token 8i + l/4.
           const uint32_t stg = smem_u32(smem_o + ew * C::kStage);
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq)
-            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
-                             stg + lane * 64 + (((qq + (lane >> 1)) & 3) * 16)),
-                         "r"(h[4 * qq]), "r"(h[4 * qq + 1]), "r"(h[4 * qq + 2]), "r"(h[4 * qq + 3])
-                         : "memory");
-          __syncwarp();
           const int64_t mw = m - lane;  // token of lane 0
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint32_t tk = 8 * i + lane / 4, pq = lane % 4;
-            const uint4 d = ld_shared_v4(stg + tk * 64 + (((pq + (tk >> 1)) & 3) * 16));
-            if (mw + tk < q.M)
-              st_global_v4(static_cast<uint16_t*>(q.out) + (mw + tk) * q.N + nb + pq * 8, d.x, d.y, d.z, d.w);
+          for (int half = 0; half < 32 / C::kStageTok; ++half) {
+            const int tl = static_cast<int>(lane) - half * C::kStageTok;  // row in the buffer
+            if (tl >= 0 && tl < C::kStageTok) {
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq)
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                 stg + tl * 64 + (((qq + (tl >> 1)) & 3) * 16)),
+                             "r"(h[4 * qq]), "r"(h[4 * qq + 1]), "r"(h[4 * qq + 2]),
+                             "r"(h[4 * qq + 3])
+                             : "memory");
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < C::kStageTok / 8; ++i) {
+              const uint32_t tk = 8 * i + lane / 4, pq = lane % 4;
+              const uint4 d = ld_shared_v4(stg + tk * 64 + (((pq + (tk >> 1)) & 3) * 16));
+              const int64_t tok = mw + half * C::kStageTok + tk;
+              if (tok < q.M)
+                st_global_v4(static_cast<uint16_t*>(q.out) + tok * q.N + nb + pq * 8, d.x, d.y,
+                             d.z, d.w);
+            }
+            __syncwarp();
           }
-          __syncwarp();
           if (tr) sp_trace(p, 11, ti);
         } else if (m_ok) {
           uint16_t* po = static_cast<uint16_t*>(q.out) + m * q.N + nb;
@@ -566,9 +578,9 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW>::kThreads, 1)
                  : "memory");
 }
 
-constexpr int kSpSX = 4, kSpNXW = 6, kSpEW = 2;
-using SpC = SpCfg<kSpSX, kSpNXW, kSpEW>;
-#define ISB_SP_KERNEL gemm_w4a8_sp<kSpSX, kSpNXW, kSpEW>
+constexpr int kSpSX = 4, kSpNXW = 6, kSpEW = 4, kSpWPB = 1;
+using SpC = SpCfg<kSpSX, kSpNXW, kSpEW, kSpWPB>;
+#define ISB_SP_KERNEL gemm_w4a8_sp<kSpSX, kSpNXW, kSpEW, kSpWPB>
 
 void launch_sp_raw(const SpMaps& maps, const SpParams& prm, int clusters, cudaStream_t s) {
   static std::once_flag once;
