@@ -208,6 +208,14 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB>::kThreads, 1)
   uint64_t* dempty = dfull + 2;     // leader: both CTAs' epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
 
+  // fold constants for k_g = 0..16, built once: a row's constants are then one 16-byte
+  // shared load instead of five conversions on the XU pipe the epilogue keeps busy
+  __shared__ uint4 fold_tab[17];
+  if (threadIdx.x < 17) {
+    const FoldK f = fold_constants(static_cast<int32_t>(threadIdx.x));
+    fold_tab[threadIdx.x] = make_uint4(f.k1, f.k16, f.cA, f.cB);
+  }
+
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();
@@ -376,7 +384,8 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB>::kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) w4[c] = ld_shared_v4(w_slot + c * (kSpWBytes / 4) + row * 16);
         const int32_t k = static_cast<int32_t>(ld_shared_u32(sc_slot + row * 4));
-        const FoldK f = fold_constants(k);
+        const uint4 fk = fold_tab[min(max(k, 0), 16)];  // k_g <= 16 on this path
+        const FoldK f{fk.x, fk.y, fk.z, fk.w};
         uint32_t a[32];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
