@@ -11,7 +11,8 @@ from oracle import oracle as O  # noqa: E402
 from tests.instances import llama_problem  # noqa: E402
 
 dev = torch.device("cuda:0")
-for m, k, n in [(16, 1024, 384), (300, 1024, 256)]:   # decode cluster kernel, prefill SS kernel
+# decode cluster kernel, prefill 1-CTA SS kernel, prefill CTA-pair kernel (ragged M and N)
+for m, k, n in [(16, 1024, 384), (300, 1024, 256), (600, 512, 384)]:
     x, w, s, xf, _ = llama_problem(m, k, n)
     pw = isb.PackedWeight.from_codes(torch.from_numpy(w.values).to(dev), 128,
                                      torch.from_numpy(w.scales).to(dev),
@@ -20,6 +21,18 @@ for m, k, n in [(16, 1024, 384), (300, 1024, 256)]:   # decode cluster kernel, p
     out = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.float32)
     assert np.array_equal(out.cpu().numpy().view(np.int32), O.gemm_integer_scale(x, w, s).output.view(np.int32))
     isb.gemm_float_scale(xq, sa, pw)
+# grouped decode launch (K1 fused) and grouped prefill launch (pair kernel)
+from bench import llama_like_weight  # noqa: E402
+gen = torch.Generator(device=dev)
+gen.manual_seed(3)
+ws = []
+for k, n in [(512, 384), (1024, 256)]:
+    c, sc = isb.quantize_weight(llama_like_weight(k, n, gen, dev), 128, 4)
+    si = isb.integerize_scales(sc.cpu().numpy(), 1024)
+    ws.append(isb.PackedWeight.from_codes(c, 128, sc, si.int_scales, 1024))
+for mm in (16, 520):
+    g = isb.GroupedGemm([{"weight": w, "x": torch.randn((mm, w.k), device=dev)} for w in ws])
+    g.run()
 xh = torch.randn((64, 512), device=dev).half()
 wh = (torch.randn((384, 512), device=dev) * 0.02).half()
 isb.gemm_dense(xh, wh)
