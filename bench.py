@@ -153,14 +153,19 @@ def llama_like_weight(k, n, gen, dev):
     return w.reshape(k, n).contiguous()
 
 
-def build_layers(isb, m, dev, seed):
+LAYER_L3_8B = [("qkv_proj", 4096, 6144), ("o_proj", 4096, 4096), ("gate_up_proj", 4096, 28672),
+               ("down_proj", 14336, 4096)]   # BASELINE configs[2] (C3): LLaMA-3-8B
+
+
+def build_layers(isb, m, dev, seed, shapes=None):
     import torch
+    shapes = shapes or LAYER
     gen = torch.Generator(device=dev)
     gen.manual_seed(seed)
     layers = []
     for _ in range(REPLICAS):
         lin = []
-        for name, k, n in LAYER:
+        for name, k, n in shapes:
             wf = llama_like_weight(k, n, gen, dev)
             codes, scales = isb.quantize_weight(wf, GROUP, 4)          # device group quantizer
             del wf
@@ -170,7 +175,7 @@ def build_layers(isb, m, dev, seed):
             del codes
             lin.append((name, k, n, w, int(s.int_scales.max())))
         layers.append(lin)
-    xs = [torch.randn((m, k), generator=gen, device=dev, dtype=torch.float32) for _, k, _ in LAYER]
+    xs = [torch.randn((m, k), generator=gen, device=dev, dtype=torch.float32) for _, k, _ in shapes]
     return layers, xs
 
 
@@ -584,6 +589,29 @@ def run_ours(args, ws, rank, local):
     if not args.no_moe:
         moe_res = moe_bench(isb, dev, args)
 
+    # ---- C3: LLaMA-3-8B decoder-layer linears, per-token act quant fused (grouped launch
+    # with K1 inside) at decode, and the grouped prefill launch at M = 2048
+    c3 = None
+    if not args.no_sweep:
+        l3, x3 = build_layers(isb, m, dev, seed=99, shapes=LAYER_L3_8B)
+        us3, _ = grouped_layer_us(isb, l3, x3, "integer-scale")
+        us3f, _ = grouped_layer_us(isb, l3, x3, "float-scale")
+        b3 = sum(alg_bytes(m, k, n, x_b=4) for _, k, n in LAYER_L3_8B)
+        xq3 = [isb.quantize_per_token(torch.randn((2048, k), device=dev)) for _, k, _ in LAYER_L3_8B]
+        us3p, _ = grouped_prefill_us(isb, l3, xq3)
+        ops3 = sum(2 * 2048 * k * n for _, k, n in LAYER_L3_8B)
+        c3 = {"workload": "llama3-8b decoder-layer linears (BASELINE configs[2]), 1 GPU",
+              "linears": [{"name": a, "K": k, "N": n} for a, k, n in LAYER_L3_8B],
+              "decode_M": m, "decode_us_per_layer": round(us3, 2),
+              "decode_float_scale_us_per_layer": round(us3f, 2),
+              "decode_hbm_frac": round(b3 / us3 / 1e3 / peak, 3),
+              "prefill_M": 2048, "prefill_us_per_layer": round(us3p, 2),
+              "prefill_tops": round(ops3 / us3p / 1e6, 1),
+              "prefill_tensor_frac_measured": round(ops3 / us3p / 1e6 / 4786.0, 3),
+              "note": "decode: one grouped launch with the per-token quantizer fused (float32 "
+                      "activations in); prefill: pre-quantized, one grouped CTA-pair launch"}
+        del l3
+
     result = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -621,6 +649,7 @@ def run_ours(args, ws, rank, local):
                      "alg_bytes_per_launch": layer_bytes, "us_per_launch": round(us_step, 3),
                      "per_linear_single_gemm": kt},
         "roofline_tensor_prefill": tensor_roof,
+        "c3_llama3_8b": c3,
         "float_scale_kernel": kf,
         "fp16_dense": {"kernel": "gemm_f16_tc (tcgen05 kind::f16, fp32 acc, no cuBLAS)",
                        "us_per_linear": [round(v, 2) for v in dense_m],
