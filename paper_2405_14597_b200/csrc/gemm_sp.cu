@@ -91,14 +91,17 @@ __device__ __forceinline__ void sp_trace(const SpParams& p, int row, int idx) {
     p.trace[(row + 16 * static_cast<int>(blockIdx.x)) * 512 + idx] = clock64_();
 }
 
-template <int SX, int NXW, int EW, int WPB>
+template <int SX, int NXW, int EW, int WPB, int WR = 1>
 struct SpCfg {
   static constexpr int kXW = NXW * WPB;  // transform warps: WPB per block slot
+  // packed-weight ring: WR slots per transform block slot (a slot always serves the same
+  // warp, so its mbarrier parity stays unambiguous), i.e. WR * NXW blocks of lookahead
+  static constexpr int kNW = WR * NXW;
   static constexpr int kEW = EW;  // epilogue warpgroups: EW / 2 per token sub-tile
   static constexpr int kThreads = 128 + 32 * kXW + 128 * kEW;
   static constexpr int kStageTok = 16;                // tokens per staging round
   static constexpr int kStage = kStageTok * 64;       // per epilogue warp: 16 tokens x 32 bf16 channels
-  static constexpr int kSmem = 1024 + SX * kSpXStage + NXW * (kSpBBytes + kSpWBytes + kSpSc) +
+  static constexpr int kSmem = 1024 + SX * kSpXStage + NXW * kSpBBytes + kNW * (kSpWBytes + kSpSc) +
                                4 * EW * kStage + 1024;
   static_assert(kSmem <= 227 * 1024, "smem");
   static_assert((4 + NXW) % 4 == 0 || true, "epilogue quadrant = warp % 4");
@@ -186,21 +189,21 @@ __device__ __forceinline__ float eq2_fast(int32_t acc, float2 s, bool& slow) {
   return f;
 }
 
-template <int SX, int NXW, int EW, int WPB>
-__global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB>::kThreads, 1)
+template <int SX, int NXW, int EW, int WPB, int WR>
+__global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
     gemm_w4a8_sp(const __grid_constant__ SpMaps maps, const __grid_constant__ SpParams p) {
-  using C = SpCfg<SX, NXW, EW, WPB>;
+  using C = SpCfg<SX, NXW, EW, WPB, WR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* smem_x = smem;                                  // [SX][2 sub-tiles][128 x 128]
   uint8_t* smem_b = smem_x + SX * kSpXStage;               // [NXW][64 x 128] folded weights
-  uint8_t* smem_w = smem_b + NXW * kSpBBytes;              // [NXW][4 chunks][64 rows][16 B]
-  uint8_t* smem_sc = smem_w + NXW * kSpWBytes;             // [NXW][64] k_g
-  uint8_t* smem_o = smem_sc + NXW * kSpSc;                 // [epilogue warp][32 x 64 B] staging
+  uint8_t* smem_w = smem_b + NXW * kSpBBytes;              // [kNW][4 chunks][64 rows][16 B]
+  uint8_t* smem_sc = smem_w + C::kNW * kSpWBytes;          // [kNW][64] k_g
+  uint8_t* smem_o = smem_sc + C::kNW * kSpSc;              // [epilogue warp][16 x 64 B] staging
   uint64_t* wfull = reinterpret_cast<uint64_t*>(smem_o + 4 * EW * C::kStage);  // local
-  uint64_t* wempty = wfull + NXW;   // local (owning transform warp)
-  uint64_t* xfull = wempty + NXW;   // leader: both CTAs' TMA bytes
+  uint64_t* wempty = wfull + C::kNW;  // local (owning transform warp)
+  uint64_t* xfull = wempty + C::kNW;  // leader: both CTAs' TMA bytes
   uint64_t* xempty = xfull + SX;    // local (multicast commit)
   uint64_t* bfull = xempty + SX;    // leader: both CTAs' transform warp
   uint64_t* bempty = bfull + NXW;   // local (multicast commit)
@@ -244,9 +247,11 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB>::kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < p.nprob; ++i) prefetch_tensormap(&maps.x[i]);
-    for (int i = 0; i < NXW; ++i) {
+    for (int i = 0; i < C::kNW; ++i) {
       mbar_init(&wfull[i], 1);
       mbar_init(&wempty[i], WPB);
+    }
+    for (int i = 0; i < NXW; ++i) {
       mbar_init(&bfull[i], 2 * WPB);
       mbar_init(&bempty[i], 1);
     }
@@ -282,8 +287,8 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB>::kThreads, 1)
         unit_of(it, pb, nt, mt);
         const SpProb& q = p.prob[pb];
         for (int kb = 0; kb < q.kblocks; ++kb, ++j) {
-          const int s = j % NXW;
-          swait(&wempty[s], ((j / NXW) & 1) ^ 1, p.dbg);
+          const int s = j % C::kNW;
+          swait(&wempty[s], ((j / C::kNW) & 1) ^ 1, p.dbg);
           mbar_arrive_expect_tx(&wfull[s], kSpWBytes + kSpSc);
           const uint8_t* src = q.packed + (static_cast<int64_t>(nt) * q.kblocks + kb) * kBlockBytes +
                                rank * (kSpWBytes / 4);
@@ -371,11 +376,14 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB>::kThreads, 1)
       unit_of(it, pb, nt, mt);
       total += p.prob[pb].kblocks;
     }
-    const uint32_t w_slot = smem_u32(smem_w + xw * kSpWBytes);
-    const uint32_t sc_slot = smem_u32(smem_sc + xw * kSpSc);
+    const uint32_t w_base = smem_u32(smem_w);
+    const uint32_t sc_base = smem_u32(smem_sc);
     const uint32_t b_slot = smem_u32(smem_b + xw * kSpBBytes);
     for (int j = xw, u = 0; j < total; j += NXW, ++u) {
-      swait(&wfull[xw], u & 1, p.dbg);
+      const int ws = j % C::kNW;  // this warp's W slots: xw, xw + NXW, ...
+      const uint32_t w_slot = w_base + ws * kSpWBytes;
+      const uint32_t sc_slot = sc_base + ws * kSpSc;
+      swait(&wfull[ws], (j / C::kNW) & 1, p.dbg);
       swait(&bempty[xw], (u & 1) ^ 1, p.dbg);
 #pragma unroll
       for (int i = 0; i < 2 / WPB; ++i) {
@@ -412,7 +420,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB>::kThreads, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&wempty[xw]);
+        mbar_arrive(&wempty[ws]);
         arrive_leader(&bfull[xw], rank);
         if (xw == 0 && half == 0) sp_trace(p, 5, u);
       }
@@ -587,9 +595,9 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB>::kThreads, 1)
                  : "memory");
 }
 
-constexpr int kSpSX = 4, kSpNXW = 6, kSpEW = 4, kSpWPB = 1;
-using SpC = SpCfg<kSpSX, kSpNXW, kSpEW, kSpWPB>;
-#define ISB_SP_KERNEL gemm_w4a8_sp<kSpSX, kSpNXW, kSpEW, kSpWPB>
+constexpr int kSpSX = 3, kSpNXW = 6, kSpEW = 4, kSpWPB = 1, kSpWR = 2;
+using SpC = SpCfg<kSpSX, kSpNXW, kSpEW, kSpWPB, kSpWR>;
+#define ISB_SP_KERNEL gemm_w4a8_sp<kSpSX, kSpNXW, kSpEW, kSpWPB, kSpWR>
 
 void launch_sp_raw(const SpMaps& maps, const SpParams& prm, int clusters, cudaStream_t s) {
   static std::once_flag once;
