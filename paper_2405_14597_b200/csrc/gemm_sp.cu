@@ -86,6 +86,10 @@ struct SpParams {
   int64_t* trace;  // debug timeline (isb_debug_set_trace): [32][512] clock64, cluster 0
 };
 
+__device__ __forceinline__ void trace_put_sp(const SpParams& p, int row, int idx, int64_t t) {
+  if (p.trace != nullptr && idx < 512 && blockIdx.x < 2)
+    p.trace[(row + 16 * static_cast<int>(blockIdx.x)) * 512 + idx] = t;
+}
 __device__ __forceinline__ void sp_trace(const SpParams& p, int row, int idx) {
   if (p.trace != nullptr && idx < 512 && blockIdx.x < 2)
     p.trace[(row + 16 * static_cast<int>(blockIdx.x)) * 512 + idx] = clock64_();
@@ -383,8 +387,12 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
       const int ws = j % C::kNW;  // this warp's W slots: xw, xw + NXW, ...
       const uint32_t w_slot = w_base + ws * kSpWBytes;
       const uint32_t sc_slot = sc_base + ws * kSpSc;
+      const bool trx = lane == 0 && warp == 4 && p.trace != nullptr;
+      const int64_t tx0 = trx ? clock64_() : 0;
       swait(&wfull[ws], (j / C::kNW) & 1, p.dbg);
+      const int64_t tx1 = trx ? clock64_() : 0;
       swait(&bempty[xw], (u & 1) ^ 1, p.dbg);
+      const int64_t tx2 = trx ? clock64_() : 0;
 #pragma unroll
       for (int i = 0; i < 2 / WPB; ++i) {
         const uint32_t row = lane + 32 * (WPB == 1 ? i : half);  // channel row of this CTA's 64
@@ -422,6 +430,12 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
       if (lane == 0) {
         mbar_arrive(&wempty[ws]);
         arrive_leader(&bfull[xw], rank);
+        if (trx) {
+          trace_put_sp(p, 12, u, tx0);
+          trace_put_sp(p, 13, u, tx1);
+          trace_put_sp(p, 14, u, tx2);
+          trace_put_sp(p, 15, u, clock64_());
+        }
         if (xw == 0 && half == 0) sp_trace(p, 5, u);
       }
     }

@@ -73,6 +73,12 @@ okc = (e8 != 0) & (e9 != 0) & (e10 != 0) & (e11 != 0)
 if okc.sum() > 4:
     print(f"epilogue chunk (warp 0): tmem ld {np.median((e9 - e8)[okc]):.0f}, convert {np.median((e10 - e9)[okc]):.0f}, "
           f"pack+stage+store {np.median((e11 - e10)[okc]):.0f}, next chunk start {np.median((e8[1:] - e11[:-1])[okc[:-1] & (e8[1:] != 0)]):.0f} (medians, cycles)")
+x12, x13, x14, x15 = t[12], t[13], t[14], t[15]
+okx = (x12 != 0) & (x15 != 0)
+if okx.sum() > 4:
+    print(f"transform warp (slot 0): wait W {np.median((x13 - x12)[okx]):.0f}, wait B slot free "
+          f"{np.median((x14 - x13)[okx]):.0f}, expand+store+arrive {np.median((x15 - x14)[okx]):.0f}, "
+          f"iteration {np.median(np.diff(x12[okx])):.0f} (medians, cycles)")
 ne = int((t[6] != 0).sum())
 for it in range(min(ne, 6)):
     tile_end = t[2][(it + 1) * kb - 1] if (it + 1) * kb - 1 < nb else 0
