@@ -171,6 +171,12 @@ int isb_gemm_act_fused_workspace_size(int64_t m, const isb_weight* w, int64_t* b
  *  - m may differ per problem (0 = no work: an expert with no routed token).
  *  - weights: group == 128, K % 128 == 0; integer path: overflow_analyzer
  *    bound within int32, else ISB_OVERFLOW (as isb_gemm_integer_scale).
+ * Routes (chosen at creation; isb_group_plan_info.tile_tokens tells which):
+ *  - every M <= 64: ONE persistent launch, K1 folded in (tile_tokens 16 / 32);
+ *  - every M >= 512, integer scale, every k_g <= 16: K1 per problem (x given) + ONE
+ *    grouped CTA-pair fold launch over all problems' tiles (tile_tokens 512);
+ *  - otherwise with some M > 64: K1 per problem + the single-GEMM kernels in turn
+ *    (tile_tokens 0).
  * The plan binds every pointer at creation (it allocates its schedule, counters
  * and any owned buffers there, never in isb_group_run) and may be replayed any
  * number of times, including inside CUDA graphs; one run at a time per plan.

@@ -263,6 +263,13 @@ void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+int64_t gemm_workspace_size(int64_t m, const isb_weight& w) { return gemm_workspace_bytes(m, w); }
+
+void gemm_dispatch(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
+                   void* out, int out_dtype, void* ws, int64_t ws_bytes, cudaStream_t s) {
+  gemm_tc(path, xq, sa, m, w.k, &w, out, out_dtype, ws, ws_bytes, s);
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("ISB_NO_PDL");

@@ -917,7 +917,7 @@ void launch_group_mt(const GMaps& maps, const GParams& prm, int grid, cudaStream
 struct GroupPlan {
   GParams prm{};
   GMaps maps{};
-  int mt = 16, path = ISB_PATH_INTEGER_SCALE, grid = 0, dev = 0, nsplit = 0;
+  int mt = 16, path = ISB_PATH_INTEGER_SCALE, grid = 0, dev = 0, nsplit = 0, out_dtype = 0;
   double makespan = 0.0;      // per-CTA budget in 128-K blocks (+ per-piece overhead)
   int* sched_dev = nullptr;   // schedule + lengths + split bases
   unsigned* sync_dev = nullptr;
@@ -926,11 +926,17 @@ struct GroupPlan {
   // Prefill route (every problem M >= kSpMinM, integer scale, k_g <= 16): K1 per problem
   // (when float activations are given) + one grouped CTA-pair fold launch (gemm_sp.cu).
   SpGroupPlan* sp = nullptr;
+  // Sequential route (some problem has M > kGroupMaxM but the pair kernel does not apply:
+  // float scale, or k_g > 16): K1 per problem + the single-GEMM prefill kernels in turn.
+  bool seq = false;
+  void* seq_ws = nullptr;
+  int64_t seq_ws_bytes = 0;
   isb_group_problem sp_probs[8] = {};  // resolved codes / scales pointers
   int sp_n = 0;
   int sp_x_dtype[8] = {};
   ~GroupPlan() {
     if (sp) sp_group_destroy(sp);
+    if (seq_ws) cudaFree(seq_ws);
     if (sched_dev) cudaFree(sched_dev);
     if (sync_dev) cudaFree(sync_dev);
     if (partials) cudaFree(partials);
@@ -939,6 +945,8 @@ struct GroupPlan {
 };
 
 namespace {
+
+constexpr int64_t kGroupMaxM = 64;  // decode grouped kernel beyond this: prefill routes
 
 int pick_group_mt(int64_t max_m) {
   return max_m <= 16 ? 16 : 32;  // 33..64 (and beyond) as 32-token tiles (gemm_tc.cu pick_mt)
@@ -1031,7 +1039,8 @@ GroupPlan* group_plan_create(const isb_group_problem* probs, int nprob, int path
   try {
     cuda_check(cudaGetDevice(&pl->dev), "cudaGetDevice");
     pl->path = path;
-    if (prefill) {
+    const bool seq = !prefill && max_m > kGroupMaxM;
+    if (prefill || seq) {
       if (own_bytes) cuda_check(cudaMalloc(&pl->owned, own_bytes), "cudaMalloc(group workspace)");
       uint8_t* own = static_cast<uint8_t*>(pl->owned);
       pl->prm.quantize = quantize;
@@ -1046,6 +1055,19 @@ GroupPlan* group_plan_create(const isb_group_problem* probs, int nprob, int path
       }
       cuda_check(cudaMalloc(&pl->sync_dev, kSyncWords * sizeof(unsigned)), "cudaMalloc(group sync)");
       cuda_check(cudaMemset(pl->sync_dev, 0, kSyncWords * sizeof(unsigned)), "cudaMemset(group sync)");
+      if (seq) {
+        pl->seq = true;
+        pl->out_dtype = out_dtype;
+        for (int i = 0; i < nprob; ++i)
+          if (probs[i].m > 0)
+            pl->seq_ws_bytes = std::max(pl->seq_ws_bytes, gemm_workspace_size(probs[i].m, *probs[i].w));
+        pl->seq_ws_bytes = std::max<int64_t>(pl->seq_ws_bytes, 256);
+        cuda_check(cudaMalloc(&pl->seq_ws, pl->seq_ws_bytes), "cudaMalloc(group gemm workspace)");
+        cuda_check(cudaMemset(pl->seq_ws, 0, pl->seq_ws_bytes), "cudaMemset(group gemm workspace)");
+        pl->grid = 1;
+        pl->mt = 0;
+        return pl;
+      }
       pl->sp = sp_group_create(pl->sp_probs, nprob, out_dtype, num_sms);
       pl->grid = 2 * (num_sms / 2);
       pl->mt = kSpTileTokens;
@@ -1206,6 +1228,18 @@ void group_plan_run(GroupPlan* pl, cudaStream_t s) {
   int dev = 0;
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   if (dev != pl->dev) fail(ISB_PARAM, "grouped GEMM plan used on another device");
+  if (pl->seq) {  // K1 per problem, then the single-GEMM kernels in turn
+    for (int i = 0; i < pl->sp_n; ++i) {
+      const isb_group_problem& q = pl->sp_probs[i];
+      if (q.m == 0) continue;
+      if (pl->prm.quantize)
+        launch_quantize_per_token(q.x, pl->sp_x_dtype[i], q.m, q.w->k, q.xq, q.sa,
+                                  reinterpret_cast<int*>(pl->sync_dev + kSyncBad), s);
+      gemm_dispatch(pl->path, q.xq, q.sa, q.m, *q.w, q.out, pl->out_dtype, pl->seq_ws,
+                    pl->seq_ws_bytes, s);
+    }
+    return;
+  }
   if (pl->sp) {
     if (pl->prm.quantize)
       for (int i = 0; i < pl->sp_n; ++i) {

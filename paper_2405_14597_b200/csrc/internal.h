@@ -123,6 +123,10 @@ void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, con
                     void* out, int out_dtype, void* workspace, const GemmPlan& plan,
                     cudaStream_t s, const void* xf = nullptr, int x_dtype = 0,
                     double* sa_out = nullptr);
+// The single-GEMM dispatch of isb_gemm_integer_scale / isb_gemm_float_scale (capi.cu).
+int64_t gemm_workspace_size(int64_t m, const isb_weight& w);
+void gemm_dispatch(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
+                   void* out, int out_dtype, void* ws, int64_t ws_bytes, cudaStream_t s);
 // Grouped layer launch (gemm_group.cu).
 struct GroupPlan;
 GroupPlan* group_plan_create(const isb_group_problem* probs, int nprob, int path, int out_dtype,

@@ -300,3 +300,30 @@ def test_group_prefill_prequantized_vs_oracle():
                 assert np.array_equal(got.astype(np.int64), ref.acc)
             else:
                 assert np.array_equal(got.view(np.int32), ref.output.view(np.int32))
+
+
+def test_group_prefill_float_and_general_integer_route_sequentially():
+    """Prefill-sized problems the pair kernel does not cover (float scale; k_g > 16 at
+    alpha = 8192) run K1 per problem + the single-GEMM prefill kernels in turn: equal to
+    the per-problem calls."""
+    from bench import llama_like_weight
+    gw = torch.Generator(device=DEV)
+    gw.manual_seed(5)
+    ws7, w8192 = [], []
+    for k, n in LLAMA2_7B[:2]:
+        codes, scales = isb.quantize_weight(llama_like_weight(k, n, gw, DEV), 128, 4)
+        for amp, dst in ((1024, ws7), (8192, w8192)):
+            si = isb.integerize_scales(scales.cpu().numpy(), amp)
+            dst.append(isb.PackedWeight.from_codes(codes, 128, scales, si.int_scales, amp))
+    assert max(w.info["max_int_scale"] for w in w8192) > 16
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(77)
+    xs = [torch.randn((600, k), generator=gen, device=DEV) for k, _ in LLAMA2_7B[:2]]
+    for path, ws in (("float-scale", ws7), ("integer-scale", w8192)):
+        g = isb.GroupedGemm([{"weight": w, "x": x} for w, x in zip(ws, xs)], path=path)
+        assert g.tile_tokens == 0  # sequential route
+        outs = g.run()
+        torch.cuda.synchronize()
+        for x, w, o in zip(xs, ws, outs):
+            _, _, ref = single_reference(x, w, path, torch.bfloat16)
+            assert torch.equal(o, ref), path
