@@ -139,15 +139,15 @@ int isb_gemm_float_scale(const int8_t* xq, const double* sa, int64_t m, int64_t 
                          int64_t workspace_bytes, void* stream);
 
 /* --------------------------------------------------------------------------
- * K1 (+) K3/K4 — per-token activation quantization fused into the GEMM
+ * K1 (+) K3/K4 — per-token activation quantization + GEMM in one call
  * (BASELINE config C3 "per-token act quant fused"): x is the float32 / bf16
- * M x K activation; each CTA quantizes its K slice into shared memory with the
- * full-row max combined across its cluster, so the codes and scales are exactly
- * those of quantize(x, 8, symmetric, per_token) (quantize.cpp:93-145) and the
- * output equals isb_quantize_per_token followed by isb_gemm_integer_scale /
- * isb_gemm_float_scale, in one launch. sa_out (nullable) receives the per-token
- * scales. Decode shapes (M <= 64) whose K slice fits run fused; anything else
- * runs the two kernels back to back (same results).
+ * M x K activation; the codes and scales are exactly those of quantize(x, 8,
+ * symmetric, per_token) (quantize.cpp:93-145) and the output equals
+ * isb_quantize_per_token followed by isb_gemm_integer_scale / isb_gemm_float_scale.
+ * sa_out (nullable) receives the per-token scales. Runs K1 into the caller's
+ * workspace then the GEMM (PDL-chained): measured faster than a single-GEMM kernel
+ * that quantizes its own K slice. The one-launch fused form is the grouped launch
+ * (isb_group_plan_*, every problem M <= 64), which quantizes inside the kernel.
  */
 int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t k,
                        const isb_weight* w, void* out, int out_dtype, double* sa_out,

@@ -451,26 +451,20 @@ int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t 
     if (out_dtype != ISB_F32 && out_dtype != ISB_BF16 && out_dtype != ISB_F16)
       fail(ISB_PARAM, "unsupported output dtype");
     cudaStream_t s = as_stream(stream);
-    const bool aligned = reinterpret_cast<uintptr_t>(x) % 16 == 0;
-    if (aligned && act_fused_eligible(m, k, *w)) {
-      const GemmPlan pl = plan_gemm(m, *w, num_sms(), path, true);
-      launch_gemm_tc(path, nullptr, nullptr, m, *w, out, out_dtype, workspace, pl, s, x, x_dtype,
-                     sa_out);
-      return;
-    }
-    // Unfused: K1 into the caller's workspace (after the GEMM's part), then the GEMM.
+    // K1 into the caller's workspace (after the GEMM's part), then the GEMM, PDL-chained:
+    // faster than a single-GEMM kernel quantizing its own slice (15.2 vs 8.3 us at M = 16,
+    // 4096 x 4096, scripts/fused_timing.py). The one-launch fused form is the grouped
+    // layer launch (isb_group_plan_*), which amortizes the quantize phase over all linears.
     const int64_t gemm_ws = gemm_workspace_bytes(m, *w);
     if (!workspace || workspace_bytes < act_fused_workspace_bytes(m, *w))
       fail(ISB_PARAM, "workspace too small: need " +
                           std::to_string(act_fused_workspace_bytes(m, *w)) +
                           " bytes (isb_gemm_act_fused_workspace_size)");
     auto* base = static_cast<uint8_t*>(workspace);
-    double* sa = reinterpret_cast<double*>(base + align256(gemm_ws));
+    // the scales go straight to sa_out when the caller wants them (no copy node)
+    double* sa = sa_out ? sa_out : reinterpret_cast<double*>(base + align256(gemm_ws));
     int8_t* codes = reinterpret_cast<int8_t*>(base + align256(gemm_ws) + align256(8 * m));
     launch_quantize_per_token(x, x_dtype, m, k, codes, sa, scratch_flag(), s);
-    if (sa_out)
-      cuda_check(cudaMemcpyAsync(sa_out, sa, m * sizeof(double), cudaMemcpyDeviceToDevice, s),
-                 "copy scales");
     gemm_tc(path, codes, sa, m, k, w, out, out_dtype, workspace, gemm_ws, stream);
   });
 }

@@ -912,12 +912,10 @@ void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, con
       default: fail(ISB_ERROR, "bad tile");
     }
   } else if (pl.fused) {
-    switch (pl.mt) {
-      ISB_DISPATCH(16, true)
-      ISB_DISPATCH(32, true)
-      ISB_DISPATCH(64, true)
-      default: fail(ISB_ERROR, "bad tile");
-    }
+    // The single-GEMM fused-quantization variant (XQ) measured slower than K1 + K3
+    // (scripts/fused_timing.py, M = 16: 15.2 vs 8.3 us at 4096 x 4096): the fused form is
+    // the grouped launch (gemm_group.cu); isb_gemm_act_fused runs K1 + K3.
+    fail(ISB_ERROR, "the single-GEMM fused-quantization kernel is not built");
   } else {
     switch (pl.mt) {
       ISB_DISPATCH(16, false)
