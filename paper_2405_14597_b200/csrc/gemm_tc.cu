@@ -263,131 +263,6 @@ __global__ void __launch_bounds__(Cfg<MT, XQ>::kThreads, 1)
       mma_commit_warp(&d_full[ds]);
     }
   } else if (warp >= 4 && warp < 4 + 4 * Cf::kXformWG) {
-    if constexpr (XQ) {
-      // ------------------------------------------------ fused per-token quantization
-      // quantize(x, 8, symmetric, per_token) (quantize.cpp:93-145) of this CTA's
-      // K slice [kb0, kb1) x 128, rows [0, MT) (decode: one token tile), into the
-      // resident SWIZZLE_128B layout the MMA reads (16 B chunk c of row r of a
-      // 128-K block lives at r*128 + ((c ^ (r & 7)) * 16)).
-      constexpr int kT = 128 * Cf::kXformWG;
-      constexpr int kTPR = kT / MT;  // threads per token row (consecutive lanes)
-      constexpr int kU = 4;          // 16-float chunks per thread kept in flight / registers
-      static_assert(kTPR >= 1 && kTPR <= 32 && (kTPR & (kTPR - 1)) == 0, "row mapping");
-      const int tid = static_cast<int>(threadIdx.x) - 128;
-      const int row = tid / kTPR, jr = tid % kTPR;
-      const int k0 = wk.kb0 * kBlockK, nblk = wk.kb1 - wk.kb0;
-      const int nch = nblk * 8;                      // 16-element chunks per row
-      const int mine = (nch - jr + kTPR - 1) / kTPR;  // chunks jr, jr + kTPR, ...
-      const bool live = row < p.M;
-      auto load_chunk = [&](int c, float (&v)[16]) {
-        const int64_t off = static_cast<int64_t>(row) * p.K + k0 + (c / 8) * kBlockK + (c % 8) * 16;
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          float t4[4];
-          if (p.x_dtype == ISB_F32)
-            load4<float>(static_cast<const float*>(p.xf) + off + h * 4, t4);
-          else
-            load4<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(p.xf) + off + h * 4, t4);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) v[h * 4 + e] = t4[e];
-        }
-      };
-      if (tid == 0) ISB_TRACE(9, 0);
-      pdl_wait();  // the activations may be produced by the preceding grid
-      if (tid == 0) ISB_TRACE(9, 1);
-      // pass 1: partial row max; the first kU chunks stay in registers for pass 2
-      float v0[kU][16];
-      float mx = 0.0f;
-      if (live) {
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (u < mine) load_chunk(jr + u * kTPR, v0[u]);
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (u < mine)
-#pragma unroll
-            for (int e = 0; e < 16; ++e) mx = fmaxf(mx, fabsf(v0[u][e]));
-        for (int u0 = kU; u0 < mine; u0 += kU) {
-          float vb[kU][16];
-#pragma unroll
-          for (int u = 0; u < kU; ++u)
-            if (u0 + u < mine) load_chunk(jr + (u0 + u) * kTPR, vb[u]);
-#pragma unroll
-          for (int u = 0; u < kU; ++u)
-            if (u0 + u < mine)
-#pragma unroll
-              for (int e = 0; e < 16; ++e) mx = fmaxf(mx, fabsf(vb[u][e]));
-        }
-      }
-#pragma unroll
-      for (int o = kTPR / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (jr == 0) amx_loc[row] = mx;
-      named_bar_sync(3, kT);
-      if (tid == 0) ISB_TRACE(9, 2);
-      if (p.C > 1) {
-        // every rank's partial maxima into every rank's amx_peer[rank][.] (DSMEM)
-        if (tid < p.C) {
-          const int q = tid;
-          for (int r = 0; r < MT; ++r)
-            asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(
-                             mapa_shared(smem_u32(amx_peer + wk.rank * MT + r), q)),
-                         "f"(amx_loc[r])
-                         : "memory");
-          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                           mapa_shared(smem_u32(amax_bar), q))
-                       : "memory");
-        }
-        mbar_wait_cluster(amax_bar, 0);
-      }
-      if (tid < MT) {
-        float a = amx_loc[tid];
-        if (p.C > 1) {
-          a = 0.0f;
-          for (int q = 0; q < p.C; ++q) a = fmaxf(a, amx_peer[q * MT + tid]);
-        }
-        const double sc = a == 0.0f ? 1.0 : static_cast<double>(a) / 127.0;  // quantize.cpp:120-125
-        sa_f[tid] = sc;
-        if (wk.rank == 0 && wk.cid == 0 && p.sa_out != nullptr && tid < p.M) p.sa_out[tid] = sc;
-      }
-      named_bar_sync(3, kT);
-      if (tid == 0) ISB_TRACE(9, 3);
-      // pass 2: codes into the resident tiles (16-byte chunk c of row r of block b at
-      // b*tile + r*128 + ((c ^ (r & 7)) * 16), the SWIZZLE_128B K-major layout)
-      const uint32_t xres = smem_u32(smem_xres);
-      const double sc = sa_f[row], rc = 1.0 / sc;
-      auto put_chunk = [&](int c, const float (&v)[16]) {
-        uint32_t w4[4] = {0u, 0u, 0u, 0u};
-        if (live) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e)
-            w4[e / 4] |= (static_cast<uint32_t>(quant_one(v[e], sc, rc, -128, 127)) & 0xFFu)
-                         << (8 * (e % 4));
-        }
-        const int b = c / 8, cb = c % 8;
-        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
-                         xres + b * Cf::kXTile + row * 128 + ((cb ^ (row & 7)) * 16)),
-                     "r"(w4[0]), "r"(w4[1]), "r"(w4[2]), "r"(w4[3])
-                     : "memory");
-      };
-#pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (u < mine) put_chunk(jr + u * kTPR, v0[u]);
-      for (int u0 = kU; u0 < mine; u0 += kU) {
-        float vb[kU][16];
-        if (live) {
-#pragma unroll
-          for (int u = 0; u < kU; ++u)
-            if (u0 + u < mine) load_chunk(jr + (u0 + u) * kTPR, vb[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (u0 + u < mine) put_chunk(jr + (u0 + u) * kTPR, vb[u]);
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
-      named_bar_sync(3, kT);
-      if (tid == 0) mbar_arrive(x_ready);
-      if (tid == 0) ISB_TRACE(9, 4);
-    }
     // ---------------------------------------------------------------- transform
     const int xw = static_cast<int>(warp - 4) / 4;
     const uint32_t r = (warp % 4) * 32 + lane;  // output channel within the tile == TMEM lane
@@ -912,10 +787,10 @@ void launch_gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, con
       default: fail(ISB_ERROR, "bad tile");
     }
   } else if (pl.fused) {
-    // The single-GEMM fused-quantization variant (XQ) measured slower than K1 + K3
-    // (scripts/fused_timing.py, M = 16: 15.2 vs 8.3 us at 4096 x 4096): the fused form is
-    // the grouped launch (gemm_group.cu); isb_gemm_act_fused runs K1 + K3.
-    fail(ISB_ERROR, "the single-GEMM fused-quantization kernel is not built");
+    // The single-GEMM fused-quantization variant (XQ, removed) measured slower than K1 +
+    // K3 (scripts/fused_timing.py, M = 16: 15.2 vs 8.3 us at 4096 x 4096): the fused form
+    // is the grouped launch (gemm_group.cu); isb_gemm_act_fused runs K1 + K3.
+    fail(ISB_ERROR, "no single-GEMM fused-quantization kernel");
   } else {
     switch (pl.mt) {
       ISB_DISPATCH(16, false)
