@@ -86,26 +86,39 @@ struct SpParams {
   int64_t* trace;  // debug timeline (isb_debug_set_trace): [32][512] clock64, cluster 0
 };
 
+// Timeline tracing (scripts/trace_pair.py) is compiled in only with -DISB_SP_TRACE=1
+// (scripts/build_sp_variant.sh): the checks cost the single-thread MMA issuer cycles.
+#ifndef ISB_SP_TRACE
+#define ISB_SP_TRACE 0
+#endif
 __device__ __forceinline__ void trace_put_sp(const SpParams& p, int row, int idx, int64_t t) {
-  if (p.trace != nullptr && idx < 512 && blockIdx.x < 2)
+  if (ISB_SP_TRACE && p.trace != nullptr && idx < 512 && blockIdx.x < 2)
     p.trace[(row + 16 * static_cast<int>(blockIdx.x)) * 512 + idx] = t;
 }
+// globaltimer rows (ns, comparable across the pair's SMs): [32 + 2 * row + cta][512]
+__device__ __forceinline__ void sp_gtrace(const SpParams& p, int row, int idx) {
+  if (ISB_SP_TRACE && p.trace != nullptr && idx < 512 && blockIdx.x < 2)
+    p.trace[(32 + 2 * row + static_cast<int>(blockIdx.x)) * 512 + idx] = globaltimer_();
+}
 __device__ __forceinline__ void sp_trace(const SpParams& p, int row, int idx) {
-  if (p.trace != nullptr && idx < 512 && blockIdx.x < 2)
+  if (ISB_SP_TRACE && p.trace != nullptr && idx < 512 && blockIdx.x < 2)
     p.trace[(row + 16 * static_cast<int>(blockIdx.x)) * 512 + idx] = clock64_();
 }
 
-template <int SX, int NXW, int EW, int WPB, int WR = 1>
+template <int SX, int NXW, int EW, int WPB, int NW, int NB>
 struct SpCfg {
-  static constexpr int kXW = NXW * WPB;  // transform warps: WPB per block slot
-  // packed-weight ring: WR slots per transform block slot (a slot always serves the same
-  // warp, so its mbarrier parity stays unambiguous), i.e. WR * NXW blocks of lookahead
-  static constexpr int kNW = WR * NXW;
+  static constexpr int kXW = NXW * WPB;  // transform warps: WPB per block (block j -> warp j % NXW)
+  // Packed-weight ring (NW blocks of lookahead) and folded-weight ring (NB slots): block j
+  // uses W slot j % NW and B slot j % NB. Both rings are at least NXW deep, so a warp's
+  // wait on a slot can never see a phase two uses old or new: its previous block's wait
+  // already covered block j - NXW - NB (MMA and producers consume in order).
+  static constexpr int kNW = NW;
+  static_assert(NW >= NXW && NB >= NXW, "rings shallower than the transform warp count");
   static constexpr int kEW = EW;  // epilogue warpgroups: EW / 2 per token sub-tile
   static constexpr int kThreads = 128 + 32 * kXW + 128 * kEW;
   static constexpr int kStageTok = 16;                // tokens per staging round
   static constexpr int kStage = kStageTok * 64;       // per epilogue warp: 16 tokens x 32 bf16 channels
-  static constexpr int kSmem = 1024 + SX * kSpXStage + NXW * kSpBBytes + kNW * (kSpWBytes + kSpSc) +
+  static constexpr int kSmem = 1024 + SX * kSpXStage + NB * kSpBBytes + kNW * (kSpWBytes + kSpSc) +
                                4 * EW * kStage + 1024;
   static_assert(kSmem <= 227 * 1024, "smem");
   static_assert((4 + NXW) % 4 == 0 || true, "epilogue quadrant = warp % 4");
@@ -193,16 +206,16 @@ __device__ __forceinline__ float eq2_fast(int32_t acc, float2 s, bool& slow) {
   return f;
 }
 
-template <int SX, int NXW, int EW, int WPB, int WR>
-__global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
+template <int SX, int NXW, int EW, int WPB, int NW, int NB>
+__global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
     gemm_w4a8_sp(const __grid_constant__ SpMaps maps, const __grid_constant__ SpParams p) {
-  using C = SpCfg<SX, NXW, EW, WPB, WR>;
+  using C = SpCfg<SX, NXW, EW, WPB, NW, NB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* smem_x = smem;                                  // [SX][2 sub-tiles][128 x 128]
-  uint8_t* smem_b = smem_x + SX * kSpXStage;               // [NXW][64 x 128] folded weights
-  uint8_t* smem_w = smem_b + NXW * kSpBBytes;              // [kNW][4 chunks][64 rows][16 B]
+  uint8_t* smem_b = smem_x + SX * kSpXStage;               // [NB][64 x 128] folded weights
+  uint8_t* smem_w = smem_b + NB * kSpBBytes;               // [kNW][4 chunks][64 rows][16 B]
   uint8_t* smem_sc = smem_w + C::kNW * kSpWBytes;          // [kNW][64] k_g
   uint8_t* smem_o = smem_sc + C::kNW * kSpSc;              // [epilogue warp][16 x 64 B] staging
   uint64_t* wfull = reinterpret_cast<uint64_t*>(smem_o + 4 * EW * C::kStage);  // local
@@ -210,8 +223,8 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
   uint64_t* xfull = wempty + C::kNW;  // leader: both CTAs' TMA bytes
   uint64_t* xempty = xfull + SX;    // local (multicast commit)
   uint64_t* bfull = xempty + SX;    // leader: both CTAs' transform warp
-  uint64_t* bempty = bfull + NXW;   // local (multicast commit)
-  uint64_t* dfull = bempty + NXW;   // local (multicast commit)
+  uint64_t* bempty = bfull + NB;    // local (multicast commit)
+  uint64_t* dfull = bempty + NB;    // local (multicast commit)
   uint64_t* dempty = dfull + 2;     // leader: both CTAs' epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
 
@@ -226,6 +239,11 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();
+  // The MMA issuer is a single thread whose per-block issue latency bounds the pipe: it
+  // sits on warp 2, whose SMSP holds one transform warp (warps 4 + 4i, 5 + 4i share
+  // SMSPs 0 / 1 with two), measured 5-6 % fewer cycles per block than on warp 1
+  // (knob 1 << 14: warp 1, A/B).
+  const uint32_t mma_warp = (p.dbg & (1 << 14)) ? 1u : 2u, alloc_warp = 3u - mma_warp;
   const int cid = static_cast<int>(blockIdx.x) / 2, ncl = static_cast<int>(gridDim.x) / 2;
   int it_begin, nunits;
   if (p.items) {
@@ -255,7 +273,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
       mbar_init(&wfull[i], 1);
       mbar_init(&wempty[i], WPB);
     }
-    for (int i = 0; i < NXW; ++i) {
+    for (int i = 0; i < NB; ++i) {
       mbar_init(&bfull[i], 2 * WPB);
       mbar_init(&bempty[i], 1);
     }
@@ -269,7 +287,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 2) {
+  if (warp == alloc_warp) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(512)
@@ -320,9 +338,12 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
         for (int kb = 0; kb < kbs; ++kb, ++j) {
           const int s = j % SX;
           swait(&xempty[s], ((j / SX) & 1) ^ 1, p.dbg);
-          if (rank == 0) mbar_arrive_expect_tx(&xfull[s], 2 * kSpXStage);  // both CTAs
+          // knob 1 << 13 (measurement): only sub-tile 0's activations are loaded (half the
+          // L2 -> SM activation traffic; sub-tile 1 computes on stale data, wrong results)
+          const int nsub = (p.dbg & (1 << 13)) ? 1 : 2;
+          if (rank == 0) mbar_arrive_expect_tx(&xfull[s], nsub * kSpXStage);  // both CTAs
 #pragma unroll
-          for (int sub = 0; sub < 2; ++sub)
+          for (int sub = 0; sub < nsub; ++sub)
             asm volatile(
                 "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
                 "bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_x + s * kSpXStage + sub * kSpXSub)),
@@ -334,11 +355,14 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp == mma_warp) {
     // ------------------------------------------------ MMA issuer (leader CTA)
     if (rank == 0 && elect_one()) {
       constexpr uint32_t idesc = make_idesc_i8(256, 128);
-      int j = 0;
+      const uint64_t adesc0 = make_sw128_kmajor_desc(smem_u32(smem_x));
+      const uint64_t bdesc0 = make_sw128_kmajor_desc(smem_u32(smem_b));
+      int j = 0, xs = 0, bs = 0;  // block, activation stage, folded-weight slot
+      uint32_t xph = 0, bph = 0;  // their ring phases
       for (int it = 0; it < nunits; ++it) {
         int pb, nt, mt;
         unit_of(it, pb, nt, mt);
@@ -348,14 +372,15 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
         tc_fence_after();
         const uint32_t d0 = tmem_base + buf * 256;
         for (int kb = 0; kb < kbs; ++kb, ++j) {
-          const int xs = j % SX, bs = j % NXW;
-          swait(&bfull[bs], (j / NXW) & 1, p.dbg);
+          swait(&bfull[bs], bph, p.dbg);
           sp_trace(p, 0, j);
-          swait(&xfull[xs], (j / SX) & 1, p.dbg);
+          sp_gtrace(p, 0, j);
+          swait(&xfull[xs], xph, p.dbg);
           sp_trace(p, 1, j);
           tc_fence_after();
-          const uint64_t bdesc = make_sw128_kmajor_desc(smem_u32(smem_b + bs * kSpBBytes));
-          const uint64_t adesc = make_sw128_kmajor_desc(smem_u32(smem_x + xs * kSpXStage));
+          // descriptors by offset from the ring bases (start-address field = addr >> 4)
+          const uint64_t bdesc = bdesc0 + static_cast<uint64_t>(bs * (kSpBBytes >> 4));
+          const uint64_t adesc = adesc0 + static_cast<uint64_t>(xs * (kSpXStage >> 4));
 #pragma unroll
           for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -365,6 +390,9 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
           commit2_mc(&xempty[xs]);
           commit2_mc(&bempty[bs]);
           sp_trace(p, 2, j);
+          sp_gtrace(p, 3, j);
+          if (++xs == SX) { xs = 0; xph ^= 1u; }
+          if (++bs == NB) { bs = 0; bph ^= 1u; }
         }
         commit2_mc(&dfull[buf]);
       }
@@ -372,7 +400,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
     __syncwarp();
   } else if (warp >= 4 && warp < 4 + C::kXW) {
     // ------------------------------------------------ transform: one warp per block
-    const int xw = (static_cast<int>(warp) - 4) / WPB;     // block slot
+    const int xw = (static_cast<int>(warp) - 4) / WPB;     // blocks j with j % NXW == xw
     const int half = (static_cast<int>(warp) - 4) % WPB;   // which rows of the slot (WPB = 2)
     int total = 0;
     for (int it = 0; it < nunits; ++it) {
@@ -382,16 +410,17 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
     }
     const uint32_t w_base = smem_u32(smem_w);
     const uint32_t sc_base = smem_u32(smem_sc);
-    const uint32_t b_slot = smem_u32(smem_b + xw * kSpBBytes);
     for (int j = xw, u = 0; j < total; j += NXW, ++u) {
-      const int ws = j % C::kNW;  // this warp's W slots: xw, xw + NXW, ...
+      const int ws = j % C::kNW, bs = j % NB;
+      const uint32_t b_slot = smem_u32(smem_b + bs * kSpBBytes);
       const uint32_t w_slot = w_base + ws * kSpWBytes;
       const uint32_t sc_slot = sc_base + ws * kSpSc;
-      const bool trx = lane == 0 && warp == 4 && p.trace != nullptr;
+      const bool trx = ISB_SP_TRACE && lane == 0 && warp == 4 && p.trace != nullptr;
       const int64_t tx0 = trx ? clock64_() : 0;
       swait(&wfull[ws], (j / C::kNW) & 1, p.dbg);
       const int64_t tx1 = trx ? clock64_() : 0;
-      swait(&bempty[xw], (u & 1) ^ 1, p.dbg);
+      swait(&bempty[bs], ((j / NB) & 1) ^ 1, p.dbg);
+      if (lane == 0) sp_gtrace(p, 1, j);
       const int64_t tx2 = trx ? clock64_() : 0;
 #pragma unroll
       for (int i = 0; i < 2 / WPB; ++i) {
@@ -429,7 +458,8 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&wempty[ws]);
-        arrive_leader(&bfull[xw], rank);
+        arrive_leader(&bfull[bs], rank);
+        sp_gtrace(p, 2, j);
         if (trx) {
           trace_put_sp(p, 12, u, tx0);
           trace_put_sp(p, 13, u, tx1);
@@ -472,7 +502,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
 #pragma unroll 1
       for (int cc = c0; cc < c0 + kChunks; ++cc) {
         uint32_t v[32];
-        const bool tr = ew == 0 && lane == 0 && p.trace != nullptr;
+        const bool tr = ISB_SP_TRACE && ew == 0 && lane == 0 && p.trace != nullptr;
         const int ti = it * 4 + cc;
         if (tr) sp_trace(p, 8, ti);
         tmem_ld_x32(taddr + cc * 32, v);
@@ -603,15 +633,21 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, WR>::kThreads, 1)
 
   tc_fence_before();
   cluster_sync_all();  // no peer arrives on our barriers after this point
-  if (warp == 2)
+  if (warp == alloc_warp)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(512)
                  : "memory");
 }
 
-constexpr int kSpSX = 3, kSpNXW = 6, kSpEW = 4, kSpWPB = 1, kSpWR = 2;
-using SpC = SpCfg<kSpSX, kSpNXW, kSpEW, kSpWPB, kSpWR>;
-#define ISB_SP_KERNEL gemm_w4a8_sp<kSpSX, kSpNXW, kSpEW, kSpWPB, kSpWR>
+#ifndef ISB_SP_NW
+#define ISB_SP_NW 10
+#endif
+#ifndef ISB_SP_NB
+#define ISB_SP_NB 8
+#endif
+constexpr int kSpSX = 3, kSpNXW = 6, kSpEW = 4, kSpWPB = 1, kSpNW = ISB_SP_NW, kSpNB = ISB_SP_NB;
+using SpC = SpCfg<kSpSX, kSpNXW, kSpEW, kSpWPB, kSpNW, kSpNB>;
+#define ISB_SP_KERNEL gemm_w4a8_sp<kSpSX, kSpNXW, kSpEW, kSpWPB, kSpNW, kSpNB>
 
 void launch_sp_raw(const SpMaps& maps, const SpParams& prm, int clusters, cudaStream_t s) {
   static std::once_flag once;

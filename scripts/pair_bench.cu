@@ -200,6 +200,210 @@ void run(const char* name, const uint8_t* src, int iters) {
   cudaFree(d);
 }
 
+
+// The prefill kernel's exact MMA stream (gemm_sp.cu): per 128-K block 8 pair MMAs
+// M=256 N=128 K=32 on two token sub-tiles (accumulators d, d+128; A sub-tiles 16 KiB
+// apart). ORDER 0: c outer / sub inner (the kernel), 1: sub outer / c inner.
+// COMMITS: 2 multicast commits per block (xempty/bempty in the kernel), nobody waits.
+// CONT (warps 4..11 while the MMA stream runs): 1 st.shared.v4 x16 + fence.proxy.async,
+// 2 tcgen05.ld 32x32b.x16 of the idle TMEM half, 3 bulk copies 8 KiB L2 -> smem (4 slots),
+// 4 st.shared.v4 x16 without the proxy fence
+template <int ORDER, int COMMITS, int CONT = 0, int WAITS = 0, int FILL = 0>
+__global__ void __launch_bounds__(384, 1) order_bench(int64_t* out, int blocks, const uint8_t* src) {
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+  // operand contents: FILL 0 zeros, 1 uniform random bytes, 2 gaussian-like int8 activations
+  // (|x| mostly < 40) and folded weights k*w4 (|.| <= 112), as the prefill kernel sees
+  for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x) {
+    uint32_t h = (i + 1) * 2654435761u;
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13; h *= 3266489917u; h ^= h >> 16;
+    uint32_t v = 0;
+    if (FILL == 1) v = h;
+    if (FILL == 2) {
+      for (int b = 0; b < 4; ++b) {
+        const int r = static_cast<int>((h >> (8 * b)) & 0xFF);
+        const int x = (i * 4 < 98304) ? (r - 128) / 4 : ((r & 15) - 8) * 7;
+        v |= (static_cast<uint32_t>(x) & 0xFFu) << (8 * b);
+      }
+    }
+    reinterpret_cast<uint32_t*>(smem)[i] = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  __shared__ uint64_t done, cb[2], bf[4], rdy[2];
+  __shared__ uint32_t slot;
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x / 32;
+  const uint32_t rank = cluster_ctarank();
+  if (threadIdx.x == 0) {
+    mbar_init(&done, 1);
+    mbar_init(&cb[0], 1);
+    mbar_init(&cb[1], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bf[i], 1);
+    mbar_init(&rdy[0], 1);
+    mbar_init(&rdy[1], 1);
+    stop = 0;
+    fence_barrier_init();
+    mbar_arrive(&rdy[0]);  // phase 0 complete: every parity-0 wait below passes at once
+    mbar_arrive(&rdy[1]);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&slot)), "r"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tb = slot;
+  constexpr uint32_t idesc = make_idesc_i8(256, 128);
+  if (warp == 1 && rank == 0 && elect_one()) {
+    const int64_t t0 = clock64_();
+    for (int j = 0; j < blocks; ++j) {
+      const int xs = j % 3, bs = j % 6;
+      const uint64_t adesc = make_sw128_kmajor_desc(smem_u32(smem + xs * 32768));
+      const uint64_t bdesc = make_sw128_kmajor_desc(smem_u32(smem + 98304 + bs * 8192));
+      const uint32_t d0 = tb + 256;
+      if (WAITS) {  // the kernel's two per-block waits (B slot, activation stage), already complete
+        mbar_wait(&rdy[0], 0);
+        mbar_wait(&rdy[1], 0);
+        tc_fence_after();
+      }
+      if (ORDER == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub)
+            mma2_ss(d0 + sub * 128, adesc + (uint64_t)(sub * (16384 >> 4) + c * 2), bdesc + (uint64_t)(c * 2), idesc);
+      } else {
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            mma2_ss(d0 + sub * 128, adesc + (uint64_t)(sub * (16384 >> 4) + c * 2), bdesc + (uint64_t)(c * 2), idesc);
+      }
+      if (COMMITS) {
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                         smem_u32(&cb[0])), "h"((uint16_t)3) : "memory");
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                         smem_u32(&cb[1])), "h"((uint16_t)3) : "memory");
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     smem_u32(&done)), "h"((uint16_t)3) : "memory");
+    mbar_wait(&done, 0);
+    if (blockIdx.x == 0) out[0] = clock64_() - t0;
+    stop = 1;
+  } else if (warp == 1 && rank == 1) {
+    mbar_wait(&done, 0);
+    stop = 1;
+  } else if (warp >= 4 && CONT != 0) {
+    const int t = threadIdx.x - 128;
+    int64_t ops = 0;
+    if (CONT == 1 || CONT == 4) {
+      const uint32_t base = smem_u32(smem + 163840) + (t * 16) % 8192;
+      while (!stop) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + q * 8192), "r"(t) : "memory");
+        if (CONT == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        ops += 4;
+      }
+    } else if (CONT == 2) {
+      const uint32_t lb = ((warp % 4) * 32) << 16;
+      uint32_t acc = 0;
+      while (!stop) {
+        uint32_t v[16];
+        tmem_ld_x16_(tb + lb + (ops * 16) % 256, v);
+        tmem_wait_ld();
+        acc ^= v[0] ^ v[15];
+        ops += 1;
+      }
+      if (acc == 0x1234567u) out[3] = acc;
+    } else if ((CONT == 3 && warp == 4) || ((CONT == 5 || CONT == 6) && warp < 8)) {
+      // bulk copies L2 -> smem: CONT 3 one warp x 4 slots; CONT 5/6 four warps x 2 slots
+      const int nq = CONT == 3 ? 4 : 2, w = warp - 4;
+      uint64_t* mb = &bf[CONT == 3 ? 0 : 0];
+      __shared__ uint64_t bfx[8];
+      if (CONT != 3) mb = &bfx[2 * w];
+      if (CONT != 3 && elect_one()) { mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); fence_barrier_init(); }
+      __syncwarp();
+      int ph[4] = {0, 0, 0, 0};
+      uint8_t* base = smem + 163840 + (CONT == 3 ? 0 : w * 16384);
+      if (elect_one()) {
+        for (int q = 0; q < nq; ++q) {
+          mbar_arrive_expect_tx(&mb[q], 8192);
+          bulk_load(base + q * 8192, src + q * 8192, 8192, &mb[q]);
+        }
+        int i = 0;
+        while (!stop) {
+          const int q = i % nq;
+          mbar_wait(&mb[q], ph[q]);
+          ph[q] ^= 1;
+          mbar_arrive_expect_tx(&mb[q], 8192);
+          bulk_load(base + q * 8192, src + (((i + w * 97) * 8192) & ((1 << 22) - 1)), 8192, &mb[q]);
+          ++i;
+          ops += 512;
+        }
+        for (int q = 0; q < nq; ++q) mbar_wait(&mb[(i + q) % nq], ph[(i + q) % nq]);
+      }
+      __syncwarp();
+    } else if (CONT == 6 && warp >= 8) {
+      const uint32_t b2 = smem_u32(smem + 163840 + 65536 - 8192) + (t * 16) % 8192;
+      while (!stop) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(b2), "r"(t) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        ops += 4 * 32;  // counted per lane below (lane 0 adds for the warp)
+      }
+    }
+    if ((threadIdx.x & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(out + 1), (unsigned long long)ops * 16);
+  }
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512) : "memory");
+}
+
+template <int ORDER, int COMMITS, int CONT = 0, int WAITS = 0, int FILL = 0>
+void run_order(const char* name, int blocks, const uint8_t* src = nullptr, int grid = 2) {
+  int64_t* d;
+  cudaMalloc(&d, 32);
+  cudaMemset(d, 0, 32);
+  auto k = order_bench<ORDER, COMMITS, CONT, WAITS, FILL>;
+  const int smem = 225 * 1024;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaLaunchKernelEx(&cfg, k, d, blocks, src);  // warm-up
+  cudaEventRecord(e0);
+  cudaLaunchKernelEx(&cfg, k, d, blocks, src);
+  cudaEventRecord(e1);
+  cudaError_t e = cudaDeviceSynchronize();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  int64_t h[2] = {0, 0};
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  const double tops = double(grid / 2) * blocks * 2.0 * 512 * 128 * 128 / (ms * 1e-3) / 1e12;
+  printf("%-34s: %7.1f cyc/block (ideal 512), side traffic %.1f B/clk, grid %d: %.0f TOPS (%s)\n", name,
+         double(h[0]) / blocks, h[0] ? double(h[1]) / double(h[0]) / 2 : 0.0, grid, tops, cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 int main() {
   uint8_t* src;
   cudaMalloc(&src, 1 << 22);
@@ -221,5 +425,34 @@ int main() {
   run<1, 0, 256, 0>("pair SS N=256", src, it);
   run<1, 0, 256, 1>("pair SS N=256 +sts", src, it);
   run<1, 0, 256, 3>("pair SS N=256 +bulk", src, it);
+  // the prefill kernel's shape (gemm_sp.cu): pair SS M=256 N=128
+  run<1, 0, 128, 0>("pair SS N=128", src, it);
+  run<1, 0, 128, 1>("pair SS N=128 +sts", src, it);
+  run<1, 0, 128, 2>("pair SS N=128 +lds", src, it);
+  run<1, 0, 128, 3>("pair SS N=128 +bulk", src, it);
+  run<0, 0, 128, 0>("1cta SS N=128", src, it);
+  run_order<0, 0>("kernel stream, c/sub order", 400);
+  run_order<0, 1>("kernel stream + commits", 400);
+  run_order<1, 0>("sub/c order", 400);
+  run_order<1, 1>("sub/c order + commits", 400);
+  run_order<0, 1, 1>("kernel stream + sts + proxy fence", 400, src);
+  run_order<0, 1, 4>("kernel stream + sts", 400, src);
+  run_order<0, 1, 2>("kernel stream + tmem ld", 400, src);
+  run_order<0, 1, 3>("kernel stream + bulk copies", 400, src);
+  run_order<0, 1, 0, 1>("stream + waits", 400, src);
+  run_order<0, 1, 1, 1>("stream + waits + sts/fence", 400, src);
+  run_order<0, 1, 4, 1>("stream + waits + sts", 400, src);
+  run_order<0, 1, 2, 1>("stream + waits + tmem ld", 400, src);
+  run_order<0, 1, 3, 1>("stream + waits + bulk", 400, src);
+  run_order<0, 1, 0, 0, 1>("stream, random bytes", 400, src);
+  run_order<0, 1, 0, 0, 2>("stream, prefill-like data", 400, src);
+  run_order<0, 1, 0, 0, 1>("stream, random bytes, 4000 blocks", 4000, src);
+  run_order<0, 1, 5, 1, 2>("stream + 4 bulk warps", 2000, src);
+  run_order<0, 1, 6, 1, 2>("stream + 4 bulk warps + sts/fence", 2000, src);
+  run_order<0, 1, 5, 1, 2>("148 SMs + 4 bulk warps", 4000, src, 148);
+  run_order<0, 1, 6, 1, 2>("148 SMs + 4 bulk warps + sts", 4000, src, 148);
+  run_order<0, 1, 0, 0, 0>("148 SMs, zeros", 20000, src, 148);
+  run_order<0, 1, 0, 0, 1>("148 SMs, random bytes", 20000, src, 148);
+  run_order<0, 1, 0, 0, 2>("148 SMs, prefill-like", 20000, src, 148);
   return 0;
 }

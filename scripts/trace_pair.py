@@ -1,6 +1,9 @@
 """Timeline of the CTA-pair prefill kernel (cluster 0, clock64): per 128-K block the MMA
 warp's a_full / xfull wait completion and issue end, the transform's wfull / a_empty
-waits, the epilogue's d_full / release. Usage: python trace_pair.py [M K N] [flags]"""
+waits, the epilogue's d_full / release. Usage: python trace_pair.py [M K N] [flags]
+Needs a library built with the timeline compiled in (the product build has none):
+  scripts/build_sp_variant.sh 10 8 $PWD/scripts/_var/sp_trace.so -DISB_SP_TRACE=1
+  ISB_LIB_PATH=$PWD/scripts/_var/sp_trace.so python scripts/trace_pair.py"""
 import ctypes as C
 import os
 import sys
@@ -29,7 +32,7 @@ lib.isb_debug_set_flags(flags | int(os.environ.get('ISB_AB_FLAG', 0)))
 for _ in range(3):
     isb.gemm_integer_scale(q, sa, w, out=out)
 torch.cuda.synchronize()
-tr = torch.zeros((32, 512), dtype=torch.int64, device=dev)
+tr = torch.zeros((48, 512), dtype=torch.int64, device=dev)
 lib.isb_debug_set_trace.argtypes = [C.c_void_p, C.c_int]
 lib.isb_debug_set_trace(C.c_void_p(tr.data_ptr()), 0)
 isb.gemm_integer_scale(q, sa, w, out=out)
@@ -73,12 +76,35 @@ okc = (e8 != 0) & (e9 != 0) & (e10 != 0) & (e11 != 0)
 if okc.sum() > 4:
     print(f"epilogue chunk (warp 0): tmem ld {np.median((e9 - e8)[okc]):.0f}, convert {np.median((e10 - e9)[okc]):.0f}, "
           f"pack+stage+store {np.median((e11 - e10)[okc]):.0f}, next chunk start {np.median((e8[1:] - e11[:-1])[okc[:-1] & (e8[1:] != 0)]):.0f} (medians, cycles)")
-x12, x13, x14, x15 = t[12], t[13], t[14], t[15]
-okx = (x12 != 0) & (x15 != 0)
-if okx.sum() > 4:
-    print(f"transform warp (slot 0): wait W {np.median((x13 - x12)[okx]):.0f}, wait B slot free "
-          f"{np.median((x14 - x13)[okx]):.0f}, expand+store+arrive {np.median((x15 - x14)[okx]):.0f}, "
-          f"iteration {np.median(np.diff(x12[okx])):.0f} (medians, cycles)")
+for base, who in ((12, "leader"), (28, "peer")):
+    x12, x13, x14, x15 = t[base], t[base + 1], t[base + 2], t[base + 3]
+    okx = (x12 != 0) & (x15 != 0)
+    if okx.sum() > 4:
+        print(f"transform warp 4 ({who}): wait W {np.median((x13 - x12)[okx]):.0f}, wait B slot free "
+              f"{np.median((x14 - x13)[okx]):.0f}, expand+store+arrive {np.median((x15 - x14)[okx]):.0f}, "
+              f"iteration {np.median(np.diff(x12[okx])):.0f} (medians, cycles)")
+# leader warp 4 handles blocks j = 6u; its B slot frees when block j - NB completes
+NB = int(os.environ.get("ISB_SP_NB_TRACE", 8))
+x14, x15 = t[14], t[15]
+us = [u for u in range(1, 512) if x14[u] and 6 * u - NB >= 0 and 6 * u < nb]
+if us:
+    dd = [x14[u] - t[2][6 * u - NB] for u in us]
+    da = [t[0][6 * u] - x15[u] for u in us if x15[u]]
+    print(f"issue(j-NB) -> slot free seen by warp (j): median {np.median(dd):.0f}; "
+          f"warp arrive(j) -> MMA bfull(j) passed: median {np.median(da):.0f} (cycles, NB={NB})")
+# globaltimer rows (ns): 32 + 2*row + cta; row 0 MMA passed bfull(j) (leader), 1 B slot free
+# seen by the transform warp of j, 2 transform arrive(j), 3 MMA issued j (leader)
+g = lambda row, cta: t[32 + 2 * row + cta]
+jj = np.arange(8, min(nb, 500))
+ok = (g(0, 0)[jj] != 0) & (g(2, 0)[jj] != 0) & (g(2, 1)[jj] != 0) & (g(1, 1)[jj] != 0)
+jj = jj[ok]
+if len(jj) > 4:
+    med = lambda a: float(np.median(a))
+    print(f"globaltimer ns (medians over {len(jj)} blocks): leader arrive -> MMA pass {med(g(0,0)[jj]-g(2,0)[jj]):.0f}, "
+          f"peer arrive -> MMA pass {med(g(0,0)[jj]-g(2,1)[jj]):.0f}; "
+          f"issue(j-NB) -> slot free at leader {med(g(1,0)[jj]-g(3,0)[jj-NB]):.0f} / peer {med(g(1,1)[jj]-g(3,0)[jj-NB]):.0f}; "
+          f"slot free -> arrive leader {med(g(2,0)[jj]-g(1,0)[jj]):.0f} / peer {med(g(2,1)[jj]-g(1,1)[jj]):.0f}; "
+          f"MMA pass -> issued {med(g(3,0)[jj]-g(0,0)[jj]):.0f}; issue-to-issue {med(np.diff(g(3,0)[jj])):.0f}")
 ne = int((t[6] != 0).sum())
 for it in range(min(ne, 6)):
     tile_end = t[2][(it + 1) * kb - 1] if (it + 1) * kb - 1 < nb else 0
