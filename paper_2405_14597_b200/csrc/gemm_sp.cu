@@ -206,6 +206,19 @@ __device__ __forceinline__ float eq2_fast(int32_t acc, float2 s, bool& slow) {
   return f;
 }
 
+// RN double -> float on the integer pipes for results in the normal float range:
+// round the 52-bit significand at bit 29 (ties to even) with one 64-bit add whose carry
+// may bump the exponent, then rebias the exponent (1023 -> 127). `ok` is false for
+// zero, subnormal-float or overflowing magnitudes (the caller uses F2F for those).
+__device__ __forceinline__ uint32_t f64_to_f32_rn_int(double x, bool& ok) {
+  const uint32_t lo = __double2loint(x), hi = static_cast<uint32_t>(__double2hiint(x));
+  const uint32_t ah = hi & 0x7FFFFFFFu;
+  ok = ah - (897u << 20) < ((1150u - 897u) << 20);  // float exponent 1..253 before rounding
+  const uint64_t t = ((static_cast<uint64_t>(ah) << 32) | lo) + 0x0FFFFFFFull + ((lo >> 29) & 1u);
+  const uint32_t r = static_cast<uint32_t>(t >> 29) - (896u << 23);
+  return r | (hi & 0x80000000u);
+}
+
 template <int SX, int NXW, int EW, int WPB, int NW, int NB>
 __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
     gemm_w4a8_sp(const __grid_constant__ SpMaps maps, const __grid_constant__ SpParams p) {
@@ -499,6 +512,91 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + lane_base + buf * 256 + sub * 128;
       const int64_t n0 = static_cast<int64_t>(nt) * kTileN;
+      if (kChunks == 2 && (q.out_dtype == ISB_BF16 || q.out_dtype == ISB_F16) &&
+          !(p.dbg & (4 | 8 | 128 | 256 | 1024 | 2048 | 4096))) {
+        // bf16 / f16 output: the second chunk's accumulators are loaded (and the TMEM
+        // buffer released to the MMA) before the first chunk's stores, so the release
+        // waits for one chunk's conversion only (knob 1024: the general loop below, A/B)
+        const bool bf = q.out_dtype == ISB_BF16;
+        auto cvt_pack = [&](const uint32_t (&v)[32], uint32_t (&h)[16]) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            // Eq. 2 exactly as gemm.cpp:252 (see the general loop below)
+            const double d0 = __hiloint2double(0x43300000, static_cast<int>(v[2 * t] ^ 0x80000000u)) -
+                              4503601774854144.0;
+            const double d1 = __hiloint2double(0x43300000, static_cast<int>(v[2 * t + 1] ^ 0x80000000u)) -
+                              4503601774854144.0;
+            float f0, f1;
+            if (p.dbg & 64) {  // A/B: double -> float rounding on the integer pipes
+              const double p0 = d0 * sa2, p1 = d1 * sa2;
+              bool ok0, ok1;
+              const uint32_t r0 = f64_to_f32_rn_int(p0, ok0), r1 = f64_to_f32_rn_int(p1, ok1);
+              f0 = ok0 ? __uint_as_float(r0) : __double2float_rn(p0);
+              f1 = ok1 ? __uint_as_float(r1) : __double2float_rn(p1);
+            } else {
+              f0 = __double2float_rn(d0 * sa2);
+              f1 = __double2float_rn(d1 * sa2);
+            }
+            if (bf) {
+              const __nv_bfloat162 b = __floats2bfloat162_rn(f0, f1);
+              h[t] = *reinterpret_cast<const uint32_t*>(&b);
+            } else {
+              const __half2 b = __floats2half2_rn(f0, f1);
+              h[t] = *reinterpret_cast<const uint32_t*>(&b);
+            }
+          }
+        };
+        auto store_h = [&](const uint32_t (&h)[16], int cc) {
+          const int64_t nb = n0 + cc * 32;
+          const int nv = q.N - nb < 32 ? static_cast<int>(q.N - nb) : 32;
+          if (nv <= 0) return;
+          if (q.N % 8 == 0 && nb + 32 <= q.N) {
+            const uint32_t stg = smem_u32(smem_o + ew * C::kStage);
+            const int64_t mw = m - lane;
+#pragma unroll
+            for (int half = 0; half < 32 / C::kStageTok; ++half) {
+              const int tl = static_cast<int>(lane) - half * C::kStageTok;
+              if (tl >= 0 && tl < C::kStageTok) {
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq)
+                  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                   stg + tl * 64 + (((qq + (tl >> 1)) & 3) * 16)),
+                               "r"(h[4 * qq]), "r"(h[4 * qq + 1]), "r"(h[4 * qq + 2]),
+                               "r"(h[4 * qq + 3])
+                               : "memory");
+              }
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < C::kStageTok / 8; ++i) {
+                const uint32_t tk = 8 * i + lane / 4, pq = lane % 4;
+                const uint4 d = ld_shared_v4(stg + tk * 64 + (((pq + (tk >> 1)) & 3) * 16));
+                const int64_t tok = mw + half * C::kStageTok + tk;
+                if (tok < q.M)
+                  st_global_v4(static_cast<uint16_t*>(q.out) + tok * q.N + nb + pq * 8, d.x, d.y, d.z, d.w);
+              }
+              __syncwarp();
+            }
+          } else if (m_ok) {
+            uint16_t* po = static_cast<uint16_t*>(q.out) + m * q.N + nb;
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+              if (t < nv) po[t] = static_cast<uint16_t>(h[t / 2] >> (16 * (t & 1)));
+          }
+        };
+        uint32_t v[32], h[16];
+        tmem_ld_x32(taddr + c0 * 32, v);
+        tmem_wait_ld();
+        cvt_pack(v, h);
+        tmem_ld_x32(taddr + (c0 + 1) * 32, v);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_leader(&dempty[buf], rank);
+        store_h(h, c0);
+        cvt_pack(v, h);
+        store_h(h, c0 + 1);
+        continue;
+      }
 #pragma unroll 1
       for (int cc = c0; cc < c0 + kChunks; ++cc) {
         uint32_t v[32];
@@ -545,6 +643,18 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
             for (int t = 0; t < 32; ++t)
               if ((slow >> t) & 1)
                 f[t] = __double2float_rn(static_cast<double>(static_cast<int32_t>(v[t])) * sa2);
+          }
+        } else if (p.dbg & 2048) {  // A/B: every int -> double on the XU pipe (I2F.F64)
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            f[t] = __double2float_rn(static_cast<double>(static_cast<int32_t>(v[t])) * sa2);
+        } else if (p.dbg & 4096) {  // A/B: int -> double alternating XU (I2F.F64) / FP64 (bias DADD)
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const double d = (t & 1) ? static_cast<double>(static_cast<int32_t>(v[t]))
+                                     : __hiloint2double(0x43300000, static_cast<int>(v[t] ^ 0x80000000u)) -
+                                           4503601774854144.0;
+            f[t] = __double2float_rn(d * sa2);
           }
         } else {
           // Eq. 2 exactly as gemm.cpp:252: (double)acc via the 2^52 + 2^31 bias (a DADD on

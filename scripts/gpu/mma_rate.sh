@@ -1,2 +1,2 @@
 #!/bin/bash
-timeout 120 ./scripts/pair_bench | grep "stream\|148"
+timeout 900 python -m pytest tests/test_gpu_group.py tests/test_gpu_scale.py tests/test_gpu_parity.py -q -x 2>&1 | tail -2

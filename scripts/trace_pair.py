@@ -48,6 +48,14 @@ iss = t[2][:nb]
 d = np.diff(iss)
 print(f"MMA issue-to-issue per block: median {np.median(d):.0f} cyc, mean {d.mean():.0f} "
       f"(ideal 512 at 256 tokens, 384 at 192)")
+print("issue-to-issue percentiles 10/25/50/75/90/99: " + " ".join(f"{np.percentile(d, q):.0f}" for q in (10, 25, 50, 75, 90, 99)))
+big = np.nonzero(d > 800)[0] + 1
+if len(big):
+    wb = t[0][big] - t[2][big - 1]
+    wxx = t[1][big] - t[0][big]
+    wi = t[2][big] - t[1][big]
+    print(f"{len(big)} of {len(d)} intervals > 800 cyc: bfull wait {np.median(wb):.0f}, xfull wait {np.median(wxx):.0f}, "
+          f"issue {np.median(wi):.0f} (medians); at kb: {np.bincount(big % kb, minlength=kb)[:8].tolist()} ...")
 wa = t[0][1:nb] - t[2][:nb - 1]
 wx = t[1][1:nb] - t[0][1:nb]
 print(f"MMA waiting a_full after prev issue: median {np.median(wa):.0f}, mean {wa.mean():.0f}; "
