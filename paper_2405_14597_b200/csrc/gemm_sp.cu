@@ -206,19 +206,6 @@ __device__ __forceinline__ float eq2_fast(int32_t acc, float2 s, bool& slow) {
   return f;
 }
 
-// RN double -> float on the integer pipes for results in the normal float range:
-// round the 52-bit significand at bit 29 (ties to even) with one 64-bit add whose carry
-// may bump the exponent, then rebias the exponent (1023 -> 127). `ok` is false for
-// zero, subnormal-float or overflowing magnitudes (the caller uses F2F for those).
-__device__ __forceinline__ uint32_t f64_to_f32_rn_int(double x, bool& ok) {
-  const uint32_t lo = __double2loint(x), hi = static_cast<uint32_t>(__double2hiint(x));
-  const uint32_t ah = hi & 0x7FFFFFFFu;
-  ok = ah - (897u << 20) < ((1150u - 897u) << 20);  // float exponent 1..253 before rounding
-  const uint64_t t = ((static_cast<uint64_t>(ah) << 32) | lo) + 0x0FFFFFFFull + ((lo >> 29) & 1u);
-  const uint32_t r = static_cast<uint32_t>(t >> 29) - (896u << 23);
-  return r | (hi & 0x80000000u);
-}
-
 template <int SX, int NXW, int EW, int WPB, int NW, int NB>
 __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
     gemm_w4a8_sp(const __grid_constant__ SpMaps maps, const __grid_constant__ SpParams p) {
@@ -526,17 +513,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
                               4503601774854144.0;
             const double d1 = __hiloint2double(0x43300000, static_cast<int>(v[2 * t + 1] ^ 0x80000000u)) -
                               4503601774854144.0;
-            float f0, f1;
-            if (p.dbg & 64) {  // A/B: double -> float rounding on the integer pipes
-              const double p0 = d0 * sa2, p1 = d1 * sa2;
-              bool ok0, ok1;
-              const uint32_t r0 = f64_to_f32_rn_int(p0, ok0), r1 = f64_to_f32_rn_int(p1, ok1);
-              f0 = ok0 ? __uint_as_float(r0) : __double2float_rn(p0);
-              f1 = ok1 ? __uint_as_float(r1) : __double2float_rn(p1);
-            } else {
-              f0 = __double2float_rn(d0 * sa2);
-              f1 = __double2float_rn(d1 * sa2);
-            }
+            const float f0 = __double2float_rn(d0 * sa2), f1 = __double2float_rn(d1 * sa2);
             if (bf) {
               const __nv_bfloat162 b = __floats2bfloat162_rn(f0, f1);
               h[t] = *reinterpret_cast<const uint32_t*>(&b);
