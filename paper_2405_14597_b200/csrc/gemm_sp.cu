@@ -239,10 +239,9 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();
-  // The MMA issuer is a single thread whose per-block issue latency bounds the pipe: it
-  // sits on warp 2, whose SMSP holds one transform warp (warps 4 + 4i, 5 + 4i share
-  // SMSPs 0 / 1 with two), measured 5-6 % fewer cycles per block than on warp 1
-  // (knob 1 << 14: warp 1, A/B).
+  // The MMA issuer is a single thread; it sits on warp 2 (knob 1 << 14: warp 1, A/B —
+  // with six transform warps, two of them sharing warp 1's SMSP, warp 2 measured 5-6 %
+  // fewer cycles per block).
   const uint32_t mma_warp = (p.dbg & (1 << 14)) ? 1u : 2u, alloc_warp = 3u - mma_warp;
   const int cid = static_cast<int>(blockIdx.x) / 2, ncl = static_cast<int>(gridDim.x) / 2;
   int it_begin, nunits;
@@ -501,19 +500,35 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
       const int64_t n0 = static_cast<int64_t>(nt) * kTileN;
       if (kChunks == 2 && (q.out_dtype == ISB_BF16 || q.out_dtype == ISB_F16) &&
           !(p.dbg & (4 | 8 | 128 | 256 | 1024 | 2048 | 4096))) {
-        // bf16 / f16 output: the second chunk's accumulators are loaded (and the TMEM
-        // buffer released to the MMA) before the first chunk's stores, so the release
-        // waits for one chunk's conversion only (knob 1024: the general loop below, A/B)
+        // bf16 / f16 output: both chunks' accumulators are loaded and the TMEM buffer is
+        // released to the MMA before any conversion (the release gates the MMA of the
+        // tile after next; 80 registers with 4 transform warps). Knob 2: the second
+        // chunk loaded after the first one's conversion; knob 1024: the general loop.
         const bool bf = q.out_dtype == ISB_BF16;
+        const double c52 = -sa2 * 4503599627370496.0;  // -2^52 * sa2, exact
         auto cvt_pack = [&](const uint32_t (&v)[32], uint32_t (&h)[16]) {
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
-            // Eq. 2 exactly as gemm.cpp:252 (see the general loop below)
-            const double d0 = __hiloint2double(0x43300000, static_cast<int>(v[2 * t] ^ 0x80000000u)) -
-                              4503601774854144.0;
-            const double d1 = __hiloint2double(0x43300000, static_cast<int>(v[2 * t + 1] ^ 0x80000000u)) -
-                              4503601774854144.0;
-            const float f0 = __double2float_rn(d0 * sa2), f1 = __double2float_rn(d1 * sa2);
+            float f0, f1;
+            if (p.dbg & 32) {  // A/B: bias DADD + DMUL (the general loop's form)
+              const double d0 = __hiloint2double(0x43300000, static_cast<int>(v[2 * t] ^ 0x80000000u)) -
+                                4503601774854144.0;
+              const double d1 = __hiloint2double(0x43300000, static_cast<int>(v[2 * t + 1] ^ 0x80000000u)) -
+                                4503601774854144.0;
+              f0 = __double2float_rn(d0 * sa2);
+              f1 = __double2float_rn(d1 * sa2);
+            } else {
+              // Eq. 2 exactly as gemm.cpp:252 in ONE FP64 op: D = 2^52 + |acc| (bit
+              // construction), fma(D, sa2, -2^52 sa2) = RN64(|acc| * sa2) — the product is
+              // exact inside the FMA and -2^52 sa2 is an exact power-of-two scaling — then
+              // F2F and the sign (RN is odd-symmetric)
+              const uint32_t a0 = v[2 * t], a1 = v[2 * t + 1];
+              const uint32_t m0 = (a0 >> 31) ? 0u - a0 : a0, m1 = (a1 >> 31) ? 0u - a1 : a1;  // |acc|
+              const double p0 = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(m0)), sa2, c52);
+              const double p1 = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(m1)), sa2, c52);
+              f0 = __uint_as_float(__float_as_uint(__double2float_rn(p0)) ^ (a0 & 0x80000000u));
+              f1 = __uint_as_float(__float_as_uint(__double2float_rn(p1)) ^ (a1 & 0x80000000u));
+            }
             if (bf) {
               const __nv_bfloat162 b = __floats2bfloat162_rn(f0, f1);
               h[t] = *reinterpret_cast<const uint32_t*>(&b);
@@ -561,6 +576,20 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
           }
         };
         uint32_t v[32], h[16];
+        if (!(p.dbg & 2)) {  // both chunks to registers, release, then convert (knob 2: A/B)
+          uint32_t w[32];
+          tmem_ld_x32(taddr + c0 * 32, v);
+          tmem_ld_x32(taddr + (c0 + 1) * 32, w);
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_leader(&dempty[buf], rank);
+          cvt_pack(v, h);
+          store_h(h, c0);
+          cvt_pack(w, h);
+          store_h(h, c0 + 1);
+          continue;
+        }
         tmem_ld_x32(taddr + c0 * 32, v);
         tmem_wait_ld();
         cvt_pack(v, h);
@@ -727,12 +756,15 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
 }
 
 #ifndef ISB_SP_NW
-#define ISB_SP_NW 10
+#define ISB_SP_NW 8
 #endif
 #ifndef ISB_SP_NB
 #define ISB_SP_NB 8
 #endif
-constexpr int kSpSX = 3, kSpNXW = 6, kSpEW = 4, kSpWPB = 1, kSpNW = ISB_SP_NW, kSpNB = ISB_SP_NB;
+#ifndef ISB_SP_NXW
+#define ISB_SP_NXW 4
+#endif
+constexpr int kSpSX = 3, kSpNXW = ISB_SP_NXW, kSpEW = 4, kSpWPB = 1, kSpNW = ISB_SP_NW, kSpNB = ISB_SP_NB;
 using SpC = SpCfg<kSpSX, kSpNXW, kSpEW, kSpWPB, kSpNW, kSpNB>;
 #define ISB_SP_KERNEL gemm_w4a8_sp<kSpSX, kSpNXW, kSpEW, kSpWPB, kSpNW, kSpNB>
 

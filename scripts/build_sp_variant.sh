@@ -7,6 +7,6 @@ cd "$(dirname "$0")/../paper_2405_14597_b200/csrc"
 make -s all
 mkdir -p _obj/var
 NVFLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 -Xcompiler -fPIC,-Wall --expt-relaxed-constexpr"
-/usr/local/cuda/bin/nvcc $NVFLAGS -DISB_SP_NW=$1 -DISB_SP_NB=$2 ${@:4} -c gemm_sp.cu -o _obj/var/gemm_sp_$1_$2.o
+/usr/local/cuda/bin/nvcc $NVFLAGS -DISB_SP_NW=$1 -DISB_SP_NB=$2 ${@:4} -c gemm_sp.cu -o _obj/var/gemm_sp_var.o
 objs=$(ls _obj/*.o | grep -v gemm_sp.o)
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$3" $objs _obj/var/gemm_sp_$1_$2.o -lcudart_static -ldl -lpthread -lrt
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$3" $objs _obj/var/gemm_sp_var.o -lcudart_static -ldl -lpthread -lrt
