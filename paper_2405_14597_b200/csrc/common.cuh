@@ -396,4 +396,32 @@ ISB_DEVICE void tmem_ld_x16_(uint32_t taddr, uint32_t (&v)[16]) {
       : "memory");
 }
 
+// Eq. 2 on the FP32 pipes: out = float((double)acc * sa2) with sa2 = s_a * 2^-e given as
+// the float pair (hi, lo), hi + lo = sa2 to ~2^-48. For |acc| < 2^22, acc is exact in
+// float, hi*acc is split exactly by FMA, and y = p1 + e approximates the exact product P
+// to ~2^-46 relative; f = RN32(y) equals RN32(RN64(P)) (the reference's two roundings,
+// gemm.cpp:252) unless P lies within ~2^-21 half-ulps of a float rounding midpoint.
+// Those outputs (and |acc| >= 2^22, out-of-range magnitudes) are flagged `slow` and
+// recomputed in FP64 by the caller — bit-identical either way, and the FP64 / conversion
+// (XU) pipes stay free of the common case.
+ISB_DEVICE float eq2_fast(int32_t acc, float2 s, bool& slow) {
+  const float a = __int_as_float(0x4B400000 + acc) - 12582912.0f;  // exact for |acc| < 2^22
+  const float p1 = __fmul_rn(a, s.x);
+  const float e1 = __fmaf_rn(a, s.x, -p1);  // exact product error
+  const float e = __fmaf_rn(a, s.y, e1);
+  const float f = __fadd_rn(p1, e);
+  const float rho = fabsf(__fsub_rn(e, __fsub_rn(f, p1)));  // |y - f|
+  const uint32_t fb = __float_as_uint(f);
+  const uint32_t E = fb & 0x7F800000u;
+  const float hu = __uint_as_float(E - (24u << 23));       // ulp(f) / 2 (normal f)
+  const float lim = (fb & 0x7FFFFFu) ? hu : 0.5f * hu;     // nearest midpoint (power of 2: below)
+  slow = static_cast<uint32_t>(acc + (1 << 22)) >= (1u << 23) ||
+         (E - (32u << 23)) > (220u << 23) || rho >= lim * (1.0f - 0x1p-18f);
+  if (acc == 0) {  // (double)0 * sa2 = +0 exactly
+    slow = false;
+    return 0.0f;
+  }
+  return f;
+}
+
 }  // namespace isb

@@ -178,33 +178,6 @@ __device__ __forceinline__ void st_global_v4(void* p, uint32_t a, uint32_t b, ui
   asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d));
 }
 
-// Eq. 2 on the FP32 pipes: out = float((double)acc * sa2) with sa2 = s_a * 2^-e given as
-// the float pair (hi, lo), hi + lo = sa2 to ~2^-48. For |acc| < 2^22, acc is exact in
-// float, hi*acc is split exactly by FMA, and y = p1 + e approximates the exact product P
-// to ~2^-46 relative; f = RN32(y) equals RN32(RN64(P)) (the reference's two roundings,
-// gemm.cpp:252) unless P lies within ~2^-21 half-ulps of a float rounding midpoint.
-// Those outputs (and |acc| >= 2^22, out-of-range magnitudes) are flagged `slow` and
-// recomputed in FP64 by the caller — bit-identical either way, and the FP64 / conversion
-// (XU) pipes stay free of the common case.
-__device__ __forceinline__ float eq2_fast(int32_t acc, float2 s, bool& slow) {
-  const float a = __int_as_float(0x4B400000 + acc) - 12582912.0f;  // exact for |acc| < 2^22
-  const float p1 = __fmul_rn(a, s.x);
-  const float e1 = __fmaf_rn(a, s.x, -p1);  // exact product error
-  const float e = __fmaf_rn(a, s.y, e1);
-  const float f = __fadd_rn(p1, e);
-  const float rho = fabsf(__fsub_rn(e, __fsub_rn(f, p1)));  // |y - f|
-  const uint32_t fb = __float_as_uint(f);
-  const uint32_t E = fb & 0x7F800000u;
-  const float hu = __uint_as_float(E - (24u << 23));       // ulp(f) / 2 (normal f)
-  const float lim = (fb & 0x7FFFFFu) ? hu : 0.5f * hu;     // nearest midpoint (power of 2: below)
-  slow = static_cast<uint32_t>(acc + (1 << 22)) >= (1u << 23) ||
-         (E - (32u << 23)) > (220u << 23) || rho >= lim * (1.0f - 0x1p-18f);
-  if (acc == 0) {  // (double)0 * sa2 = +0 exactly
-    slow = false;
-    return 0.0f;
-  }
-  return f;
-}
 
 template <int SX, int NXW, int EW, int WPB, int NW, int NB>
 __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
@@ -478,6 +451,21 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
     const uint32_t qd = warp % 4;  // a warp reaches TMEM lanes 32 * (warp % 4) ..
     const uint32_t lane_base = (qd * 32) << 16;
     pdl_wait();
+    // this thread's token scale, fetched one tile ahead: under the prefill's L2 load a
+    // demand load issued at the tile boundary stalled the first conversion ~5 k cycles
+    auto token_of = [&](int it, int64_t& m, const SpProb*& qq) {
+      int pb, nt, mt;
+      unit_of(it, pb, nt, mt);
+      qq = &p.prob[pb];
+      m = static_cast<int64_t>(mt) * kSpT + sub * 256 + rank * 128 + qd * 32 + lane;
+    };
+    double sa_next = 0.0;
+    if (nunits > 0) {
+      int64_t m1;
+      const SpProb* q1;
+      token_of(0, m1, q1);
+      sa_next = m1 < q1->M ? __ldg(q1->sa + m1) : 0.0;
+    }
     for (int it = 0; it < nunits; ++it) {
       int pb, nt, mt;
       unit_of(it, pb, nt, mt);
@@ -485,13 +473,12 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
       const int buf = it & 1;
       const int64_t m = static_cast<int64_t>(mt) * kSpT + sub * 256 + rank * 128 + qd * 32 + lane;
       const bool m_ok = m < q.M;
-      const double sa2 = m_ok ? __ldg(q.sa + m) * q.inv_amp : 0.0;  // s_a * 2^-e, exact
-      float2 sf2;  // (hi, lo) float split of sa2 for eq2_fast; hi = NaN: always the exact path
-      {
-        const float hi = __double2float_rn(sa2);
-        const bool ok = fabs(sa2) >= 0x1p-100 && fabs(sa2) <= 0x1p100;
-        sf2 = make_float2(ok ? hi : __int_as_float(0x7FC00000),
-                          __double2float_rn(sa2 - static_cast<double>(hi)));
+      const double sa2 = sa_next * q.inv_amp;  // s_a * 2^-e, exact (0 past M)
+      if (it + 1 < nunits) {
+        int64_t m1;
+        const SpProb* q1;
+        token_of(it + 1, m1, q1);
+        sa_next = m1 < q1->M ? __ldg(q1->sa + m1) : 0.0;
       }
       swait(&dfull[buf], (it >> 1) & 1, p.dbg);
       if (ew == 0 && lane == 0) sp_trace(p, 6, it);
@@ -506,11 +493,30 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
         // chunk loaded after the first one's conversion; knob 1024: the general loop.
         const bool bf = q.out_dtype == ISB_BF16;
         const double c52 = -sa2 * 4503599627370496.0;  // -2^52 * sa2, exact
+        const bool dadd_form = p.dbg & 32;
         auto cvt_pack = [&](const uint32_t (&v)[32], uint32_t (&h)[16]) {
+          if (dadd_form) {  // A/B: bias DADD + DMUL (the general loop's form)
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              const double d0 = __hiloint2double(0x43300000, static_cast<int>(v[2 * t] ^ 0x80000000u)) -
+                                4503601774854144.0;
+              const double d1 = __hiloint2double(0x43300000, static_cast<int>(v[2 * t + 1] ^ 0x80000000u)) -
+                                4503601774854144.0;
+              const float f0 = __double2float_rn(d0 * sa2), f1 = __double2float_rn(d1 * sa2);
+              if (bf) {
+                const __nv_bfloat162 b = __floats2bfloat162_rn(f0, f1);
+                h[t] = *reinterpret_cast<const uint32_t*>(&b);
+              } else {
+                const __half2 b = __floats2half2_rn(f0, f1);
+                h[t] = *reinterpret_cast<const uint32_t*>(&b);
+              }
+            }
+            return;
+          }
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
             float f0, f1;
-            if (p.dbg & 32) {  // A/B: bias DADD + DMUL (the general loop's form)
+            if (false) {
               const double d0 = __hiloint2double(0x43300000, static_cast<int>(v[2 * t] ^ 0x80000000u)) -
                                 4503601774854144.0;
               const double d1 = __hiloint2double(0x43300000, static_cast<int>(v[2 * t + 1] ^ 0x80000000u)) -
@@ -578,16 +584,33 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
         uint32_t v[32], h[16];
         if (!(p.dbg & 2)) {  // both chunks to registers, release, then convert (knob 2: A/B)
           uint32_t w[32];
+          // timeline (trace builds): clock64 kept in registers, written after the tile
+          const bool tr = ISB_SP_TRACE && ew == 0 && lane == 0 && p.trace != nullptr;
+          int64_t ts[6] = {0, 0, 0, 0, 0, 0};
+          if (tr) ts[0] = clock64_();
           tmem_ld_x32(taddr + c0 * 32, v);
           tmem_ld_x32(taddr + (c0 + 1) * 32, w);
           tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) arrive_leader(&dempty[buf], rank);
+          if (tr) ts[1] = clock64_() + (v[0] == 0x7fffffffu ? 1 : 0);
           cvt_pack(v, h);
+          if (tr) ts[2] = clock64_() + (h[15] == 0x7fffffffu ? 1 : 0);
           store_h(h, c0);
+          if (tr) ts[3] = clock64_();
           cvt_pack(w, h);
+          if (tr) ts[4] = clock64_() + (h[15] == 0x7fffffffu ? 1 : 0);
           store_h(h, c0 + 1);
+          if (tr) {
+            ts[5] = clock64_();
+            trace_put_sp(p, 8, it * 4, ts[0]);
+            trace_put_sp(p, 9, it * 4, ts[1]);
+            trace_put_sp(p, 10, it * 4, ts[2]);
+            trace_put_sp(p, 11, it * 4, ts[3]);
+            trace_put_sp(p, 8, it * 4 + 1, ts[4]);
+            trace_put_sp(p, 9, it * 4 + 1, ts[5]);
+          }
           continue;
         }
         tmem_ld_x32(taddr + c0 * 32, v);
@@ -637,6 +660,13 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
 #pragma unroll
           for (int t = 0; t < 32; ++t) f[t] = __int_as_float(v[t]);
         } else if (p.dbg & 256) {  // A/B: FP32 fast path with exact FP64 fallback (eq2_fast)
+          float2 sf2;  // (hi, lo) float split of sa2; hi = NaN: always the exact path
+          {
+            const float hi = __double2float_rn(sa2);
+            const bool ok = fabs(sa2) >= 0x1p-100 && fabs(sa2) <= 0x1p100;
+            sf2 = make_float2(ok ? hi : __int_as_float(0x7FC00000),
+                              __double2float_rn(sa2 - static_cast<double>(hi)));
+          }
           uint32_t slow = 0;
 #pragma unroll
           for (int t = 0; t < 32; ++t) {

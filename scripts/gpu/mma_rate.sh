@@ -1,3 +1,3 @@
 #!/bin/bash
-timeout 120 python scripts/pf_time.py 2048 0 32 0 32
-timeout 100 python scripts/pair_quick.py 2048 2>&1 | grep -v "== ss: True" | head -4
+timeout 120 python scripts/pf_time.py 2048 0
+timeout 900 python -m pytest tests/test_gpu_group.py tests/test_gpu_scale.py tests/test_gpu_parity.py -q -x 2>&1 | tail -2

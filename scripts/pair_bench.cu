@@ -404,6 +404,134 @@ void run_order(const char* name, int blocks, const uint8_t* src = nullptr, int g
   cudaFree(d);
 }
 
+// Does the FP64 pipe (the Eq. 2 conversion: DFMA + F2F.F32.F64) slow down while the
+// tensor core runs a kind::i8 MMA stream in the same SM pair? 16 warps convert register
+// data (ILP 8) for `iters` rounds; MMA: 0 idle, 1 the prefill kernel's MMA stream.
+__device__ __forceinline__ float eq2_fast_b(int32_t acc, float2 s, bool& slow) {
+  const float a = __int_as_float(0x4B400000 + acc) - 12582912.0f;
+  const float p1 = __fmul_rn(a, s.x);
+  const float e1 = __fmaf_rn(a, s.x, -p1);
+  const float e = __fmaf_rn(a, s.y, e1);
+  const float f = __fadd_rn(p1, e);
+  const float rho = fabsf(__fsub_rn(e, __fsub_rn(f, p1)));
+  const uint32_t fb = __float_as_uint(f);
+  const uint32_t E = fb & 0x7F800000u;
+  const float hu = __uint_as_float(E - (24u << 23));
+  const float lim = (fb & 0x7FFFFFu) ? hu : 0.5f * hu;
+  slow = static_cast<uint32_t>(acc + (1 << 22)) >= (1u << 23) || (E - (32u << 23)) > (220u << 23) ||
+         rho >= lim * (1.0f - 0x1p-18f);
+  return f;
+}
+
+template <int MMA, int FORM = 0>
+__global__ void __launch_bounds__(640, 1) cvt_mma_bench(int64_t* out, int iters) {
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t done;
+  __shared__ uint32_t slot;
+  __shared__ volatile int stop;
+  __shared__ int finished;
+  const int warp = threadIdx.x / 32;
+  const uint32_t rank = cluster_ctarank();
+  if (threadIdx.x == 0) {
+    mbar_init(&done, 1);
+    stop = 0;
+    finished = 0;
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tb = slot;
+  if (warp == 1 && rank == 0 && MMA) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = make_idesc_i8(256, 128);
+      const uint64_t adesc = make_sw128_kmajor_desc(smem_u32(smem));
+      const uint64_t bdesc = make_sw128_kmajor_desc(smem_u32(smem + 98304));
+      int j = 0;
+      while (!stop) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub)
+            mma2_ss(tb + 256 + sub * 128, adesc + (uint64_t)(sub * 1024 + c * 2), bdesc + (uint64_t)(c * 2), idesc);
+        if (++j % 8 == 0) {  // bound the queue: wait for the stream every 8 blocks
+          asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                           smem_u32(&done)), "h"((uint16_t)3) : "memory");
+          mbar_wait(&done, ((j / 8) - 1) & 1);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    uint32_t a[8];
+    for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 977u + i * 131071u;
+    const double sa2 = 1.0e-3 + threadIdx.x * 1e-9, c52 = -sa2 * 4503599627370496.0;
+    uint32_t acc = 0;
+    __syncwarp();
+    const int64_t t0 = clock64_();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t f;
+        if (FORM == 0) {
+          const uint32_t m = (a[i] >> 31) ? 0u - a[i] : a[i];
+          const double pr = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(m)), sa2, c52);
+          f = __float_as_uint(__double2float_rn(pr)) ^ (a[i] & 0x80000000u);
+        } else {
+          bool sl;
+          const float2 sf = make_float2(__double2float_rn(sa2), 0.0f);
+          f = __float_as_uint(eq2_fast_b(static_cast<int32_t>(a[i] & 0x3FFFFFu), sf, sl)) ^ (sl ? 1u : 0u);
+        }
+        acc += f;
+        a[i] += f * 2654435761u;
+      }
+    }
+    const int64_t t1 = clock64_();
+    if (acc == 0x1234567u) out[3] = acc;
+    if ((threadIdx.x & 31) == 0) {
+      if (blockIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)(t1 - t0));
+      if (atomicAdd(&finished, 1) == 15) stop = 1;
+    }
+  }
+  __syncthreads();
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512) : "memory");
+}
+
+template <int MMA, int FORM = 0>
+void run_cvt(const char* name, int iters) {
+  int64_t* d;
+  cudaMalloc(&d, 32);
+  cudaMemset(d, 0, 32);
+  auto k = cvt_mma_bench<MMA, FORM>;
+  const int smem = 160 * 1024;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2);
+  cfg.blockDim = dim3(640);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, d, iters);
+  cudaError_t e = cudaDeviceSynchronize();
+  int64_t h = 0;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("%-34s: %.2f conversions / clk / SM (%s)\n", name, 512.0 * iters * 8 / double(h), cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 int main() {
   uint8_t* src;
   cudaMalloc(&src, 1 << 22);
@@ -451,6 +579,10 @@ int main() {
   run_order<0, 1, 6, 1, 2>("stream + 4 bulk warps + sts/fence", 2000, src);
   run_order<0, 1, 5, 1, 2>("148 SMs + 4 bulk warps", 4000, src, 148);
   run_order<0, 1, 6, 1, 2>("148 SMs + 4 bulk warps + sts", 4000, src, 148);
+  run_cvt<0>("Eq.2 DFMA form, tensor idle", 2000);
+  run_cvt<1>("Eq.2 DFMA form, i8 MMA stream", 2000);
+  run_cvt<0, 1>("Eq.2 FP32 eq2_fast, tensor idle", 2000);
+  run_cvt<1, 1>("Eq.2 FP32 eq2_fast, i8 MMA stream", 2000);
   run_order<0, 1, 0, 0, 0>("148 SMs, zeros", 20000, src, 148);
   run_order<0, 1, 0, 0, 1>("148 SMs, random bytes", 20000, src, 148);
   run_order<0, 1, 0, 0, 2>("148 SMs, prefill-like", 20000, src, 148);

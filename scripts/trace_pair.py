@@ -84,6 +84,17 @@ okc = (e8 != 0) & (e9 != 0) & (e10 != 0) & (e11 != 0)
 if okc.sum() > 4:
     print(f"epilogue chunk (warp 0): tmem ld {np.median((e9 - e8)[okc]):.0f}, convert {np.median((e10 - e9)[okc]):.0f}, "
           f"pack+stage+store {np.median((e11 - e10)[okc]):.0f}, next chunk start {np.median((e8[1:] - e11[:-1])[okc[:-1] & (e8[1:] != 0)]):.0f} (medians, cycles)")
+# fast bf16 epilogue path (warp ew 0): rows 8/9/10/11 at index 4*it and 8/9 at 4*it+1
+ii = [i for i in range(0, 120) if t[8][4 * i] and t[9][4 * i] and t[10][4 * i] and t[11][4 * i] and t[8][4 * i + 1] and t[9][4 * i + 1]]
+if len(ii) > 2:
+    e = lambda r, o: np.array([t[r][4 * i + o] for i in ii], dtype=np.int64)
+    ld, ca, sa_, cb, sb = e(9, 0) - e(8, 0), e(10, 0) - e(9, 0), e(11, 0) - e(10, 0), e(8, 1) - e(11, 0), e(9, 1) - e(8, 1)
+    print(f"fast epilogue per tile (warp 0, medians, cycles): ld+release {np.median(ld):.0f}, convert A {np.median(ca):.0f}, "
+          f"store A {np.median(sa_):.0f}, convert B {np.median(cb):.0f}, store B {np.median(sb):.0f}; "
+          f"tile starts {[int(t[8][4 * i] - t0) for i in ii[:6]]}")
+    if t[3][ii[0]]:
+        c1 = np.array([t[3][i] for i in ii]) - e(9, 0)
+        print(f"  convert A twice: first pass {np.median(c1):.0f}, second {np.median(e(10, 0) - np.array([t[3][i] for i in ii])):.0f}")
 for base, who in ((12, "leader"), (28, "peer")):
     x12, x13, x14, x15 = t[base], t[base + 1], t[base + 2], t[base + 3]
     okx = (x12 != 0) & (x15 != 0)
