@@ -742,38 +742,6 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
       for (int t = 0; t < MT; ++t)
         sav[t] = PATH == ISB_PATH_INTEGER_SCALE ? sa_t[t] * q.inv_amp : sa_t[t];
       uint32_t res[2][MT];
-      if (PATH == ISB_PATH_INTEGER_SCALE && q.out_dtype != ISB_I32 && (p.dbg & (1 << 16))) {
-        // A/B: Eq. 2 on the FP32 pipes (eq2_fast), exact FP64 redo of flagged outputs
-        uint64_t slow = 0;
-#pragma unroll
-        for (int t = 0; t < MT; ++t) {
-          const float hi = __double2float_rn(sav[t]);
-          const bool ok = fabs(sav[t]) >= 0x1p-100 && fabs(sav[t]) <= 0x1p100;
-          const float2 sf = make_float2(ok ? hi : __int_as_float(0x7FC00000),
-                                        __double2float_rn(sav[t] - static_cast<double>(hi)));
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            bool sl;
-            const float f = eq2_fast(static_cast<int32_t>(acc[h][t]), sf, sl);
-            slow |= sl ? (1ull << t) : 0ull;
-            res[h][t] = ob == 4 ? __float_as_uint(f)
-                        : q.out_dtype == ISB_BF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(f))
-                                                  : __half_as_ushort(__float2half_rn(f));
-          }
-        }
-        if (slow) {
-#pragma unroll
-          for (int t = 0; t < MT; ++t)
-            if ((slow >> t) & 1ull)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const float f = finish_eq<PATH>(static_cast<int32_t>(acc[h][t]), 0.0f, sav[t]);
-                res[h][t] = ob == 4 ? __float_as_uint(f)
-                            : q.out_dtype == ISB_BF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(f))
-                                                      : __half_as_ushort(__float2half_rn(f));
-              }
-        }
-      } else
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll

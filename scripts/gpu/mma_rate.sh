@@ -1,3 +1,2 @@
 #!/bin/bash
-timeout 120 python scripts/pf_time.py 2048 0
-timeout 900 python -m pytest tests/test_gpu_group.py tests/test_gpu_scale.py tests/test_gpu_parity.py -q -x 2>&1 | tail -2
+for m in 16 32 64; do timeout 300 python scripts/group_knobs.py $m 65536; done
