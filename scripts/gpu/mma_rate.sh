@@ -1,2 +1,3 @@
 #!/bin/bash
-for m in 16 32 64; do timeout 300 python scripts/group_knobs.py $m 65536; done
+timeout 120 python scripts/pf_time.py 2048 0 64 0 64
+timeout 100 python scripts/pair_quick.py 2048 64 2>&1 | grep -v "== ss: True" | head -4
