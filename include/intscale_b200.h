@@ -122,11 +122,14 @@ int isb_weight_info(const isb_weight* w, isb_weight_info_t* info);
  * xq: int8 codes M x K; sa: double[M]. out: M x N in out_dtype.
  * Requires K % 128 == 0 and group % 128 == 0 (isb_weight_info.tensor_core_ok);
  * other shapes => ISB_PARAM (use isb_gemm_checked).
- * Overflow gate: the integer path accumulates in int32, which is exact iff the
+ * Overflow: the integer path accumulates in int32, which is exact iff the
  * weight's overflow_analyzer bound (analysis.cpp:24-59, computed at pack time)
- * fits int32; an unsafe weight returns ISB_OVERFLOW instead of wrapping (the
- * exact int64 path is isb_gemm_checked; run_layer falls back to float scale,
- * gemm.cpp:489-516).
+ * fits int32. An unsafe weight runs as the fewest equal K-chunks (by groups,
+ * at most 16) whose own bounds fit int32: per-chunk int32 accumulators in the
+ * workspace, then one exact int64 sum + Eq. 2 — the reference's int64 result
+ * (gemm.cpp:205-262). ISB_OVERFLOW only for raw int32 output (cannot hold the
+ * sum) or a layer no such split makes safe (exact scalar path:
+ * isb_gemm_checked; run_layer falls back to float scale, gemm.cpp:489-516).
  * workspace: caller-owned device buffer of isb_gemm_workspace_size() bytes,
  * zero-filled once before first use (the kernels leave it zeroed).
  */
@@ -170,7 +173,8 @@ int isb_gemm_act_fused_workspace_size(int64_t m, const isb_weight* w, int64_t* b
  *  - x == NULL (every problem): xq / sa are the int8 codes and double scales.
  *  - m may differ per problem (0 = no work: an expert with no routed token).
  *  - weights: group == 128, K % 128 == 0; integer path: overflow_analyzer
- *    bound within int32, else ISB_OVERFLOW (as isb_gemm_integer_scale).
+ *    bound within int32, else ISB_OVERFLOW (the K-chunked exact path of
+ *    isb_gemm_integer_scale is single-GEMM only).
  * Routes (chosen at creation; isb_group_plan_info.tile_tokens tells which):
  *  - every M <= 64: ONE persistent launch, K1 folded in (tile_tokens 16 / 32);
  *  - every M >= 512, integer scale, every k_g <= 16: K1 per problem (x given) + ONE

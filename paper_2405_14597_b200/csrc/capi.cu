@@ -145,6 +145,25 @@ isb_weight* pack_common(const int16_t* codes, const uint8_t* s4, int64_t k, int6
         worst = std::max(worst, col);
       }
       w->static_bound = worst;
+      // K-chunking for unsafe layers: the fewest equal group ranges whose bounds fit int32
+      w->safe_chunks = 1;
+      if (worst > std::numeric_limits<int32_t>::max()) {
+        w->safe_chunks = 0;
+        for (int c = 2; c <= kMaxChunks && c <= w->groups; ++c) {
+          int64_t wc = 0;
+          for (int64_t col = 0; col < n && wc <= std::numeric_limits<int32_t>::max(); ++col)
+            for (int q = 0; q < c; ++q) {
+              int64_t b = 0;
+              for (int64_t g = q * w->groups / c; g < (q + 1) * w->groups / c; ++g)
+                b += group * 127 * 8 * static_cast<int64_t>(h[static_cast<size_t>(col * w->groups + g)]);
+              wc = std::max(wc, b);
+            }
+          if (wc <= std::numeric_limits<int32_t>::max()) {
+            w->safe_chunks = c;
+            break;
+          }
+        }
+      }
     }
     DeviceFlag bad(s);
     launch_pack(codes, s4, k, n, w->packed, w->kblocks, w->n_tiles, bad.d, s);
@@ -188,10 +207,18 @@ bool pg_disabled() {
 
 int64_t align256(int64_t b) { return (b + 255) / 256 * 256; }
 
+// Unsafe layers (static bound > int32) on the integer path: K-chunk accumulators.
+bool chunked_exact(const isb_weight& w) {
+  return w.static_bound > std::numeric_limits<int32_t>::max() && w.safe_chunks > 1 &&
+         w.tensor_core_ok() && w.group == kBlockK;
+}
+
 int64_t gemm_workspace_bytes(int64_t m, const isb_weight& w) {
   if (!w.tensor_core_ok()) return 0;
-  return std::max(plan_gemm(m, w, num_sms(), ISB_PATH_INTEGER_SCALE).workspace_bytes,
-                  plan_gemm(m, w, num_sms(), ISB_PATH_FLOAT_SCALE).workspace_bytes);
+  int64_t b = std::max(plan_gemm(m, w, num_sms(), ISB_PATH_INTEGER_SCALE).workspace_bytes,
+                       plan_gemm(m, w, num_sms(), ISB_PATH_FLOAT_SCALE).workspace_bytes);
+  if (chunked_exact(w)) b = std::max<int64_t>(b, int64_t{w.safe_chunks} * m * w.n * 4);
+  return b;
 }
 
 // act-fused two-kernel form: GEMM workspace, then s_a [m] doubles, then codes [m][k].
@@ -216,10 +243,13 @@ void require_gemm_args(const int8_t* xq, const double* sa, int64_t m, int64_t k,
 // the int32 split-K exchange). That equals the reference's int64 acc only while
 // overflow_analyzer's static bound fits int32 (analysis.cpp:24-59); otherwise the
 // device sum could wrap where the reference flags / throws (gemm.cpp:42-52, :90-98).
-// Unsafe layers are refused with ISB_OVERFLOW: the exact int64 path is
-// isb_gemm_checked, and run_layer's float-scale fallback (gemm.cpp:489-516).
-void require_int32_safe(const isb_weight* w) {
-  if (w->static_bound > std::numeric_limits<int32_t>::max())
+// Unsafe layers run as K-chunks whose own bounds fit int32 (raw int32 accumulators per
+// chunk, then an exact int64 sum + Eq. 2: finalize_chunks_kernel); only layers no split
+// up to kMaxChunks makes safe, and raw int32 output (which cannot hold the sum), are
+// refused with ISB_OVERFLOW (the exact scalar path is isb_gemm_checked).
+void require_int32_safe(const isb_weight* w, int out_dtype) {
+  if (w->static_bound > std::numeric_limits<int32_t>::max() &&
+      (out_dtype == ISB_I32 || !chunked_exact(*w)))
     fail(ISB_OVERFLOW, "static overflow bound " + std::to_string(w->static_bound) +
                            " exceeds int32: the tensor-core integer-scale GEMM cannot be exact "
                            "for this layer (use isb_gemm_checked or the float-scale fallback)");
@@ -235,9 +265,26 @@ void gemm_tc(int path, const int8_t* xq, const double* sa, int64_t m, int64_t k,
     fail(ISB_PARAM, "integer-scale path needs an IntegerScaleSet");
   if (out_dtype == ISB_I32 && path != ISB_PATH_INTEGER_SCALE)
     fail(ISB_PARAM, "raw int32 accumulator output exists only on the integer-scale path");
-  if (path == ISB_PATH_INTEGER_SCALE) require_int32_safe(w);
+  if (path == ISB_PATH_INTEGER_SCALE) require_int32_safe(w, out_dtype);
   if (m > std::numeric_limits<int>::max() || w->n > std::numeric_limits<int>::max())
     fail(ISB_PARAM, "shape too large");
+  if (path == ISB_PATH_INTEGER_SCALE && chunked_exact(*w)) {
+    // the exact tensor-core path of an unsafe layer: C per-group-epilogue launches over
+    // equal group ranges into int32 chunk accumulators, one int64 sum + Eq. 2 launch
+    const int c = w->safe_chunks;
+    const int64_t need = int64_t{c} * m * w->n * 4;
+    if (!ws || ws_bytes < need)
+      fail(ISB_PARAM, "workspace too small: need " + std::to_string(need) + " bytes");
+    int32_t* acc = static_cast<int32_t*>(ws);
+    for (int q = 0; q < c; ++q) {
+      const int64_t g0 = q * w->groups / c, g1 = (q + 1) * w->groups / c;
+      launch_gemm_pg(path, xq, sa, m, *w, acc + q * m * w->n, ISB_I32, num_sms(), as_stream(stream),
+                     g0, g1 - g0);
+    }
+    launch_finalize_chunks(acc, c, sa, m, w->n, std::ldexp(1.0, -w->exponent), out, out_dtype,
+                           as_stream(stream));
+    return;
+  }
   const GemmPlan pl = plan_gemm(m, *w, num_sms(), path);
   if (!ws || ws_bytes < pl.workspace_bytes)
     fail(ISB_PARAM, "workspace too small: need " + std::to_string(pl.workspace_bytes) + " bytes");
@@ -447,7 +494,7 @@ int isb_gemm_act_fused(int path, const void* x, int x_dtype, int64_t m, int64_t 
       fail(ISB_PARAM, "unknown path");
     if (path == ISB_PATH_INTEGER_SCALE && !w->has_int_scales)
       fail(ISB_PARAM, "integer-scale path needs an IntegerScaleSet");
-    if (path == ISB_PATH_INTEGER_SCALE) require_int32_safe(w);
+    if (path == ISB_PATH_INTEGER_SCALE) require_int32_safe(w, out_dtype);
     if (out_dtype != ISB_F32 && out_dtype != ISB_BF16 && out_dtype != ISB_F16)
       fail(ISB_PARAM, "unsupported output dtype");
     cudaStream_t s = as_stream(stream);

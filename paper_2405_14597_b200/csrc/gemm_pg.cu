@@ -56,6 +56,7 @@ struct PgParams {
   const double* sa;       // [M]
   void* out;              // [M][N]
   int M, N, G, kblocks, m_tiles, tiles, out_dtype, late_shift;
+  int kb0, kbw;  // first 128-K block of this launch, the weight's block count (K-chunked calls)
   double inv_amp;
 };
 
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         tile_of(j / p.kblocks, nt, mt);
         mbar_arrive_expect_tx(&wfull[s], kBlockBytes);
         bulk_load_evict_first(smem_w + s * kBlockBytes,
-                              p.packed + (static_cast<int64_t>(nt) * p.kblocks + j % p.kblocks) *
+                              p.packed + (static_cast<int64_t>(nt) * p.kbw + p.kb0 + j % p.kblocks) *
                                              kBlockBytes,
                               kBlockBytes, &wfull[s]);
       }
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         tile_of(j / p.kblocks, nt, mt);
         mbar_arrive_expect_tx(&s_full[s], kTileN * 4);
         bulk_load(smem_sc + s * kTileN * 4,
-                  p.scale + (static_cast<int64_t>(nt) * p.G + j % p.kblocks) * kTileN, kTileN * 4,
+                  p.scale + (static_cast<int64_t>(nt) * p.G + p.kb0 + j % p.kblocks) * kTileN, kTileN * 4,
                   &s_full[s]);
       }
     }
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         int nt, mt;
         tile_of(j / p.kblocks, nt, mt);
         mbar_arrive_expect_tx(&xfull[s], kPgXBytes);
-        tma_load_2d(smem_x + s * kPgXBytes, &x_map, &xfull[s], (j % p.kblocks) * kBlockK,
+        tma_load_2d(smem_x + s * kPgXBytes, &x_map, &xfull[s], (p.kb0 + j % p.kblocks) * kBlockK,
                     mt * kPgMT);
       }
     }
@@ -370,7 +371,8 @@ bool pg_eligible(int64_t m, const isb_weight& w) {
 }
 
 void launch_gemm_pg(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
-                    void* out, int out_dtype, int num_sms, cudaStream_t s) {
+                    void* out, int out_dtype, int num_sms, cudaStream_t s, int64_t kb0, int64_t kbn) {
+  if (kbn < 0) kbn = w.kblocks - kb0;
   PgParams prm{};
   prm.packed = w.packed;
   prm.scale = path == ISB_PATH_INTEGER_SCALE ? w.kscale_tiled
@@ -380,12 +382,14 @@ void launch_gemm_pg(int path, const int8_t* xq, const double* sa, int64_t m, con
   prm.M = static_cast<int>(m);
   prm.N = static_cast<int>(w.n);
   prm.G = static_cast<int>(w.groups);
-  prm.kblocks = static_cast<int>(w.kblocks);
+  prm.kblocks = static_cast<int>(kbn);
+  prm.kb0 = static_cast<int>(kb0);
+  prm.kbw = static_cast<int>(w.kblocks);
   prm.m_tiles = static_cast<int>((m + kPgMT - 1) / kPgMT);
   prm.tiles = static_cast<int>(w.n_tiles) * prm.m_tiles;
   prm.out_dtype = out_dtype;
   prm.late_shift = (path == ISB_PATH_INTEGER_SCALE && w.static_bound > 0 &&
-                    w.static_bound <= (int64_t{1} << 27) - 1) ? 1 : 0;
+                    w.static_bound <= (int64_t{1} << 27) - 1 && kbn == w.kblocks) ? 1 : 0;
   prm.inv_amp = std::ldexp(1.0, -w.exponent);
   const CUtensorMap map = make_x_map(xq, m, w.k, kPgMT);
   const int grid = std::min(prm.tiles, num_sms);

@@ -16,6 +16,9 @@ struct isb_weight {
   int32_t has_int_scales = 0;
   int32_t max_int_scale = 0;
   int64_t static_bound = 0;  // overflow_analyzer bound of the int scales (analysis.cpp:24-59)
+  // fewest equal K-chunks (by groups) whose own bounds fit int32 (1 when static_bound does;
+  // 0 when none up to kMaxChunks does): the exact tensor-core path for unsafe layers
+  int32_t safe_chunks = 1;
   int64_t kblocks = 0;   // ceil(K / 128)
   int64_t n_tiles = 0;   // ceil(N / 128)
   uint8_t* packed = nullptr;        // n_tiles * kblocks * 8 KiB
@@ -62,6 +65,8 @@ void launch_row_absmax(const void* x, int x_dtype, int64_t m, int64_t k, float* 
                        cudaStream_t s);
 void launch_quantize_amax(const void* x, int x_dtype, int64_t m, int64_t k, const float* amax,
                           int8_t* codes, double* scales, cudaStream_t s);
+void launch_finalize_chunks(int32_t* acc, int chunks, const double* sa, int64_t m, int64_t n,
+                            double inv_amp, void* out, int out_dtype, cudaStream_t s);
 void launch_finalize_acc(const int32_t* acc, const double* sa, int64_t m, int64_t n,
                          double inv_amp, void* out, int out_dtype, cudaStream_t s);
 
@@ -102,9 +107,13 @@ double sp_group_balance(const SpGroupPlan* pl);
 void sp_group_destroy(SpGroupPlan* pl);
 // Prefill per-group-epilogue K3 (any k_g) / K4 on the SS skeleton (gemm_pg.cu).
 constexpr int64_t kPgMinM = 128;
+constexpr int kMaxChunks = 16;  // K-chunk limit of the exact tensor-core path for unsafe layers
 bool pg_eligible(int64_t m, const isb_weight& w);
+// kb0 / kbn: the 128-K blocks [kb0, kb0 + kbn) of the weight (kbn < 0: all), for the
+// K-chunked exact path of unsafe layers (ISB_I32 raw chunk accumulators).
 void launch_gemm_pg(int path, const int8_t* xq, const double* sa, int64_t m, const isb_weight& w,
-                    void* out, int out_dtype, int num_sms, cudaStream_t s);
+                    void* out, int out_dtype, int num_sms, cudaStream_t s, int64_t kb0 = 0,
+                    int64_t kbn = -1);
 // Dense fp16/bf16 baseline (gemm_f16.cu): out = x[M][K] * w[N][K]^T, K % 64 == 0.
 void launch_gemm_dense(const void* x, const void* w, int64_t m, int64_t n, int64_t k, void* out,
                        int out_dtype, bool bf16, int num_sms, cudaStream_t s);

@@ -115,6 +115,33 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Unsafe layers (static bound > int32): the GEMM runs as C K-chunks whose own bounds
+// fit int32 (raw accumulators in acc[c][m][n]); the exact int64 sum of the chunks is the
+// reference's acc (gemm.cpp:205-262 accumulates in int64), then Eq. 2 as above
+// (double(acc) is exact below 2^53).
+__global__ void __launch_bounds__(kThreads)
+    finalize_chunks_kernel(int32_t* __restrict__ acc, int chunks, const double* __restrict__ sa,
+                           int64_t m, int64_t n, double inv_amp, void* __restrict__ out, int dtype) {
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();
+  const int64_t total = m * n;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * kThreads) {
+    int64_t a = 0;
+    for (int c = 0; c < chunks; ++c) {
+      int32_t* pc = acc + c * total + idx;
+      a += *pc;
+      *pc = 0;  // the GEMM workspace is handed back zeroed (isb_gemm_workspace_size contract)
+    }
+    const int64_t i = idx / n;
+    const double o = __dmul_rn(static_cast<double>(a) * inv_amp, sa[i]);
+    const float f = __double2float_rn(o);
+    if (dtype == ISB_F32) static_cast<float*>(out)[idx] = f;
+    else if (dtype == ISB_BF16) static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(f);
+    else static_cast<__half*>(out)[idx] = __float2half_rn(f);
+  }
+}
+
 template <typename K, typename... Args>
 void launch_opt(bool pdl, K kern, dim3 grid, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg{};
@@ -185,6 +212,13 @@ void launch_finalize_acc(const int32_t* acc, const double* sa, int64_t m, int64_
   const int64_t blocks = std::min<int64_t>((m * n + kThreads - 1) / kThreads, 148 * 16);
   launch_pdl(finalize_acc_kernel, dim3(static_cast<unsigned>(std::max<int64_t>(blocks, 1))), s,
              acc, sa, m, n, inv_amp, out, out_dtype);
+}
+
+void launch_finalize_chunks(int32_t* acc, int chunks, const double* sa, int64_t m, int64_t n,
+                            double inv_amp, void* out, int out_dtype, cudaStream_t s) {
+  const int64_t blocks = std::min<int64_t>((m * n + kThreads - 1) / kThreads, 148 * 16);
+  launch_pdl(finalize_chunks_kernel, dim3(static_cast<unsigned>(std::max<int64_t>(blocks, 1))), s,
+             acc, chunks, sa, m, n, inv_amp, out, out_dtype);
 }
 
 }  // namespace isb

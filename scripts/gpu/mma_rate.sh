@@ -1,3 +1,3 @@
 #!/bin/bash
-timeout 120 python scripts/pf_time.py 2048 0 64 0 64
-timeout 100 python scripts/pair_quick.py 2048 64 2>&1 | grep -v "== ss: True" | head -4
+timeout 1500 python -m pytest tests/ -q -x -m gpu 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2

@@ -12,7 +12,8 @@
   integer below 2^53, so any summation order is exact), and the float32 output must
   equal the reference epilogue float((double(acc) / 2^e) * s_a) (gemm.cpp:252)
   applied to it — bit for bit.
-* The overflow gate: an unsafe layer (static bound > int32) is refused.
+* Unsafe layers (static bound > int32): the K-chunked exact tensor-core path equals the
+  reference's int64 result; raw int32 output stays refused.
 * K1 on rows whose absmax is below 127 / FLT_MAX.
 """
 import functools
@@ -280,27 +281,57 @@ def test_decode_split_k_dsmem_stress(c):
 
 
 # ------------------------------------------------------------------------- overflow gate
-def test_unsafe_layer_is_refused_not_wrapped():
+def test_unsafe_layer_runs_k_chunked_exact():
     """OverflowRig-scale layer (test_gemm.cpp:345-383): x = 127, w = -8 codes, k = 1170
-    over K = 4096 has a static bound of 4.26e9 > int32: the tensor-core integer path
-    must refuse it (ISB_OVERFLOW) instead of returning a wrapped sum; the checked
-    kernel returns the exact int64 result; the float-scale path still runs."""
+    over K = 4096 has a static bound of 4.26e9 > int32. The tensor-core integer path
+    runs it as K-chunks whose bounds fit int32 plus an exact int64 sum (the reference
+    accumulates in int64, gemm.cpp:205-262): float32 output bit-equal to the oracle's.
+    Raw int32 output cannot hold the sum and stays refused (ISB_OVERFLOW); the checked
+    kernel returns the exact int64 accumulator with the overflow flagged."""
     from tests.instances import overflow_rig
     x, w, s = overflow_rig(256)
     assert not O.overflow_analyzer(4096, 128, 8, 4, s)["safe"]
     pw = pack(w, s)
     xq, sa = dev(x.values, torch.int8), dev(x.scales)
-    for dt in (torch.float32, torch.bfloat16, torch.int32):
-        with pytest.raises(isb.OverflowError_):
-            isb.gemm_integer_scale(xq, sa, pw, out_dtype=dt)
-    xf = dev(np.full((1, 4096), 127.0, np.float32))
+    ref = O.gemm_integer_scale(x, w, s)
+    out = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(out.view(np.uint32), ref.output.view(np.uint32))
+    ob = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.bfloat16).float().cpu().numpy()
+    assert np.array_equal(ob, bf16_np(ref.output))
     with pytest.raises(isb.OverflowError_):
-        isb.gemm_act_fused(xf, pw, out_dtype=torch.float32)
+        isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.int32)
+    xf = dev(np.full((1, 4096), 127.0, np.float32))
+    of = isb.gemm_act_fused(xf, pw, out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(of.view(np.uint32), ref.output.view(np.uint32))
     _, _, acc, _, st = isb.gemm_checked("integer-scale", xq, sa, pw)
     assert acc.cpu().numpy()[0, 0] == -4260372480 and st["overflow_detected"]
     rf = O.gemm_float_scale(x, w)
     out = isb.gemm_float_scale(xq, sa, pw, out_dtype=torch.float32).cpu().numpy()
     assert np.allclose(out, rf.output, rtol=1e-5)
+
+
+@pytest.mark.parametrize("m", [1, 300])
+def test_unsafe_random_layer_k_chunked_matches_oracle(m):
+    """A random layer made unsafe by a large amplifier (alpha = 2^12: k_g in the
+    hundreds to thousands, static bound several times int32): several K-chunks,
+    ragged M."""
+    rng = np.random.default_rng(11)
+    xf = rng.standard_normal((m, 4096)).astype(np.float32)
+    wf = (rng.standard_normal((4096, 384)) * rng.uniform(0.2, 2.0, (1, 384))).astype(np.float32)
+    x = O.quantize_per_token(xf)
+    w = O.quantize_weight(wf, 128)
+    s = O.integerize_scales(w.scales, 1 << 12)
+    b = O.overflow_analyzer(4096, 128, 8, 4, s)
+    assert not b["safe"] and 2 ** 32 < b["static_bound"] < 8 * 2 ** 31
+    pw = pack(w, s)
+    xq, sa = dev(x.values, torch.int8), dev(x.scales)
+    ref = O.gemm_integer_scale(x, w, s)
+    assert np.abs(ref.acc).max() < 2 ** 53
+    for _ in range(3):  # repeated launches: the chunk buffers are reused
+        out = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.float32).cpu().numpy()
+        assert np.array_equal(out.view(np.uint32), ref.output.view(np.uint32))
+    ob = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.bfloat16).float().cpu().numpy()
+    assert np.array_equal(ob, bf16_np(ref.output))
 
 
 # ------------------------------------------------------------------------- K1 tiny rows
