@@ -309,7 +309,9 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         for (int t = 0; t < kCols; ++t) iacc[t] >>= 4;  // exact: 16 | acc16
       }
       cp_async_wait<1>();
-      named_bar_sync(1, 128 * kPgEW);  // sa_s[it & 1] landed for every thread
+      // integer path: s_a * 2^-e once per token (exact), not once per output
+      if (PATH == ISB_PATH_INTEGER_SCALE && te < kPgMT) sa_s[(it & 1) * kPgMT + te] *= p.inv_amp;
+      named_bar_sync(1, 128 * kPgEW);  // sa_s[it & 1] landed (and scaled) for every thread
       const double* sa_t = sa_s + (it & 1) * kPgMT + g * kCols;
       const int64_t n = static_cast<int64_t>(nt) * kTileN + r;
       const int64_t m0 = static_cast<int64_t>(mt) * kPgMT + g * kCols;
@@ -323,8 +325,21 @@ __global__ void __launch_bounds__(kPgThreads, 1)
               if (p.out_dtype == ISB_I32) {
                 static_cast<int32_t*>(p.out)[idx] = iacc[t];
               } else {
-                const double o = __dmul_rn(static_cast<double>(iacc[t]), sa_t[t] * p.inv_amp);
-                pg_store(p.out, p.out_dtype, idx, __double2float_rn(o));
+                // Eq. 2 in one FP64 op (the FP64 pipe is the epilogue's scarce resource
+                // while the tensor core streams): D = 2^52 + |acc| by bit construction,
+                // fma(D, sa2, -2^52 sa2) = RN64(|acc| * sa2) exactly, sign after F2F
+                const double sa2 = sa_t[t];
+                const uint32_t a = static_cast<uint32_t>(iacc[t]);
+                const uint32_t mag = (a >> 31) ? 0u - a : a;
+                // -2^52 * sa2 by exponent arithmetic (ALU), DMUL only for zero / subnormal sa2
+                const int sh = __double2hiint(sa2);
+                const double c52 = (sh & 0x7FF00000) != 0 && (sh & 0x7FF00000) < 0x7C000000
+                                       ? __hiloint2double((sh + (52 << 20)) ^ static_cast<int>(0x80000000u),
+                                                          __double2loint(sa2))
+                                       : -sa2 * 4503599627370496.0;
+                const double o = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(mag)), sa2, c52);
+                pg_store(p.out, p.out_dtype, idx,
+                         __uint_as_float(__float_as_uint(__double2float_rn(o)) ^ (a & 0x80000000u)));
               }
             } else {
               const double o = __dmul_rn(static_cast<double>(facc[t]), sa_t[t]);

@@ -1,3 +1,3 @@
 #!/bin/bash
-timeout 1500 python -m pytest tests/ -q -x -m gpu 2>&1 | tail -3
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
+for m in 16 32 64; do timeout 300 python scripts/group_knobs.py $m; done
+timeout 900 python -m pytest tests/test_gpu_group.py -q -x 2>&1 | tail -2
