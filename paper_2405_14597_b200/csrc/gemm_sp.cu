@@ -91,6 +91,9 @@ struct SpParams {
 #ifndef ISB_SP_TRACE
 #define ISB_SP_TRACE 0
 #endif
+#ifndef ISB_SP_KNOBS
+#define ISB_SP_KNOBS 0
+#endif
 __device__ __forceinline__ void trace_put_sp(const SpParams& p, int row, int idx, int64_t t) {
   if (ISB_SP_TRACE && p.trace != nullptr && idx < 512 && blockIdx.x < 2)
     p.trace[(row + 16 * static_cast<int>(blockIdx.x)) * 512 + idx] = t;
@@ -201,6 +204,11 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
   uint64_t* dempty = dfull + 2;     // leader: both CTAs' epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
 
+  // Measurement knobs (isb_debug_set_flags) are compiled in only with -DISB_SP_KNOBS=1
+  // (scripts/build_sp_variant.sh): their dead branches otherwise cost the product
+  // epilogue registers (spills in the staged-store loop).
+  const int dbg = ISB_SP_KNOBS ? p.dbg : 0;
+
   // fold constants for k_g = 0..16, built once: a row's constants are then one 16-byte
   // shared load instead of five conversions on the XU pipe the epilogue keeps busy
   __shared__ uint4 fold_tab[17];
@@ -215,7 +223,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
   // The MMA issuer is a single thread; it sits on warp 2 (knob 1 << 14: warp 1, A/B —
   // with six transform warps, two of them sharing warp 1's SMSP, warp 2 measured 5-6 %
   // fewer cycles per block).
-  const uint32_t mma_warp = (p.dbg & (1 << 14)) ? 1u : 2u, alloc_warp = 3u - mma_warp;
+  const uint32_t mma_warp = (dbg & (1 << 14)) ? 1u : 2u, alloc_warp = 3u - mma_warp;
   const int cid = static_cast<int>(blockIdx.x) / 2, ncl = static_cast<int>(gridDim.x) / 2;
   int it_begin, nunits;
   if (p.items) {
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
         const SpProb& q = p.prob[pb];
         for (int kb = 0; kb < q.kblocks; ++kb, ++j) {
           const int s = j % C::kNW;
-          swait(&wempty[s], ((j / C::kNW) & 1) ^ 1, p.dbg);
+          swait(&wempty[s], ((j / C::kNW) & 1) ^ 1, dbg);
           mbar_arrive_expect_tx(&wfull[s], kSpWBytes + kSpSc);
           const uint8_t* src = q.packed + (static_cast<int64_t>(nt) * q.kblocks + kb) * kBlockBytes +
                                rank * (kSpWBytes / 4);
@@ -309,10 +317,10 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
         const int kbs = p.prob[pb].kblocks;
         for (int kb = 0; kb < kbs; ++kb, ++j) {
           const int s = j % SX;
-          swait(&xempty[s], ((j / SX) & 1) ^ 1, p.dbg);
+          swait(&xempty[s], ((j / SX) & 1) ^ 1, dbg);
           // knob 1 << 13 (measurement): only sub-tile 0's activations are loaded (half the
           // L2 -> SM activation traffic; sub-tile 1 computes on stale data, wrong results)
-          const int nsub = (p.dbg & (1 << 13)) ? 1 : 2;
+          const int nsub = (dbg & (1 << 13)) ? 1 : 2;
           if (rank == 0) mbar_arrive_expect_tx(&xfull[s], nsub * kSpXStage);  // both CTAs
 #pragma unroll
           for (int sub = 0; sub < nsub; ++sub)
@@ -340,14 +348,14 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
         unit_of(it, pb, nt, mt);
         const int kbs = p.prob[pb].kblocks;
         const int buf = it & 1;
-        swait(&dempty[buf], ((it >> 1) & 1) ^ 1, p.dbg);
+        swait(&dempty[buf], ((it >> 1) & 1) ^ 1, dbg);
         tc_fence_after();
         const uint32_t d0 = tmem_base + buf * 256;
         for (int kb = 0; kb < kbs; ++kb, ++j) {
-          swait(&bfull[bs], bph, p.dbg);
+          swait(&bfull[bs], bph, dbg);
           sp_trace(p, 0, j);
           sp_gtrace(p, 0, j);
-          swait(&xfull[xs], xph, p.dbg);
+          swait(&xfull[xs], xph, dbg);
           sp_trace(p, 1, j);
           tc_fence_after();
           // descriptors by offset from the ring bases (start-address field = addr >> 4)
@@ -389,9 +397,9 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
       const uint32_t sc_slot = sc_base + ws * kSpSc;
       const bool trx = ISB_SP_TRACE && lane == 0 && warp == 4 && p.trace != nullptr;
       const int64_t tx0 = trx ? clock64_() : 0;
-      swait(&wfull[ws], (j / C::kNW) & 1, p.dbg);
+      swait(&wfull[ws], (j / C::kNW) & 1, dbg);
       const int64_t tx1 = trx ? clock64_() : 0;
-      swait(&bempty[bs], ((j / NB) & 1) ^ 1, p.dbg);
+      swait(&bempty[bs], ((j / NB) & 1) ^ 1, dbg);
       if (lane == 0) sp_gtrace(p, 1, j);
       const int64_t tx2 = trx ? clock64_() : 0;
 #pragma unroll
@@ -409,7 +417,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
           const uint32_t wv[4] = {w4[c].x, w4[c].y, w4[c].z, w4[c].w};
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
-            if (p.dbg & 1) {  // measurement: no fold ALU (wrong results)
+            if (dbg & 1) {  // measurement: no fold ALU (wrong results)
               a[c * 8 + 2 * w] = wv[w] ^ f.k1;
               a[c * 8 + 2 * w + 1] = wv[w];
             } else {
@@ -480,20 +488,20 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
         token_of(it + 1, m1, q1);
         sa_next = m1 < q1->M ? __ldg(q1->sa + m1) : 0.0;
       }
-      swait(&dfull[buf], (it >> 1) & 1, p.dbg);
+      swait(&dfull[buf], (it >> 1) & 1, dbg);
       if (ew == 0 && lane == 0) sp_trace(p, 6, it);
       tc_fence_after();
       const uint32_t taddr = tmem_base + lane_base + buf * 256 + sub * 128;
       const int64_t n0 = static_cast<int64_t>(nt) * kTileN;
       if (kChunks == 2 && (q.out_dtype == ISB_BF16 || q.out_dtype == ISB_F16) &&
-          !(p.dbg & (4 | 8 | 128 | 256 | 1024 | 2048 | 4096))) {
+          !(dbg & (4 | 8 | 128 | 256 | 1024 | 2048 | 4096))) {
         // bf16 / f16 output: both chunks' accumulators are loaded and the TMEM buffer is
         // released to the MMA before any conversion (the release gates the MMA of the
         // tile after next; 80 registers with 4 transform warps). Knob 2: the second
         // chunk loaded after the first one's conversion; knob 1024: the general loop.
         const bool bf = q.out_dtype == ISB_BF16;
         const double c52 = -sa2 * 4503599627370496.0;  // -2^52 * sa2, exact
-        const bool dadd_form = p.dbg & 32;
+        const bool dadd_form = dbg & 32;
         auto cvt_pack = [&](const uint32_t (&v)[32], uint32_t (&h)[16]) {
           if (dadd_form) {  // A/B: bias DADD + DMUL (the general loop's form)
 #pragma unroll
@@ -582,7 +590,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
           }
         };
         uint32_t v[32], h[16];
-        if (!(p.dbg & 2)) {  // both chunks to registers, release, then convert (knob 2: A/B)
+        if (!(dbg & 2)) {  // both chunks to registers, release, then convert (knob 2: A/B)
           uint32_t w[32];
           // timeline (trace builds): clock64 kept in registers, written after the tile
           const bool tr = ISB_SP_TRACE && ew == 0 && lane == 0 && p.trace != nullptr;
@@ -641,7 +649,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
           if (lane == 0) arrive_leader(&dempty[buf], rank);
           if (ew == 0 && lane == 0) sp_trace(p, 7, it);
         }
-        if (p.dbg & 4) continue;  // (lanes past M stay: the staged store below is warp-wide)
+        if (dbg & 4) continue;  // (lanes past M stay: the staged store below is warp-wide)
         const int64_t nb = n0 + cc * 32;
         const int nv = q.N - nb < 32 ? static_cast<int>(q.N - nb) : 32;  // valid channels
         if (nv <= 0) continue;
@@ -656,10 +664,10 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
         // Eq. 2 exactly as gemm.cpp:252: (double)acc via the 2^52 + 2^31 bias (a DADD on
         // the FP64 pipe instead of an I2F.F64 conversion), one DMUL, one F2F.F32.F64
         float f[32];
-        if (p.dbg & 8) {  // measurement: no conversion (wrong results)
+        if (dbg & 8) {  // measurement: no conversion (wrong results)
 #pragma unroll
           for (int t = 0; t < 32; ++t) f[t] = __int_as_float(v[t]);
-        } else if (p.dbg & 256) {  // A/B: FP32 fast path with exact FP64 fallback (eq2_fast)
+        } else if (dbg & 256) {  // A/B: FP32 fast path with exact FP64 fallback (eq2_fast)
           float2 sf2;  // (hi, lo) float split of sa2; hi = NaN: always the exact path
           {
             const float hi = __double2float_rn(sa2);
@@ -680,11 +688,11 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
               if ((slow >> t) & 1)
                 f[t] = __double2float_rn(static_cast<double>(static_cast<int32_t>(v[t])) * sa2);
           }
-        } else if (p.dbg & 2048) {  // A/B: every int -> double on the XU pipe (I2F.F64)
+        } else if (dbg & 2048) {  // A/B: every int -> double on the XU pipe (I2F.F64)
 #pragma unroll
           for (int t = 0; t < 32; ++t)
             f[t] = __double2float_rn(static_cast<double>(static_cast<int32_t>(v[t])) * sa2);
-        } else if (p.dbg & 4096) {  // A/B: int -> double alternating XU (I2F.F64) / FP64 (bias DADD)
+        } else if (dbg & 4096) {  // A/B: int -> double alternating XU (I2F.F64) / FP64 (bias DADD)
 #pragma unroll
           for (int t = 0; t < 32; ++t) {
             const double d = (t & 1) ? static_cast<double>(static_cast<int32_t>(v[t]))
@@ -731,7 +739,7 @@ __global__ void __launch_bounds__(SpCfg<SX, NXW, EW, WPB, NW, NB>::kThreads, 1)
             h[t] = *reinterpret_cast<const uint32_t*>(&b);
           }
         }
-        if (p.dbg & 128) {  // measurement: no stores (wrong results)
+        if (dbg & 128) {  // measurement: no stores (wrong results)
           if ((h[0] ^ h[7] ^ h[15]) == 0x12345u && m_ok) static_cast<uint16_t*>(q.out)[m * q.N + nb] = 0;
           continue;
         }

@@ -1,5 +1,6 @@
 """Tiny driver for ncu captures of one kernel: K3/K4 on a single shape, weights
-rotated over 3 replicas. Usage: python scripts/prof_gemm.py M K N [int|float] [iters]"""
+rotated over 3 replicas. Usage: python scripts/prof_gemm.py M K N [int|float] [iters]
+(ISB_ALPHA=8192 for the general per-group integer path, k_g up to ~124)"""
 import os
 import sys
 
@@ -22,8 +23,9 @@ ws = []
 for _ in range(3):
     wf = bench.llama_like_weight(k, n, gen, dev)
     codes, scales = isb.quantize_weight(wf, 128, 4)
-    s = isb.integerize_scales(scales.cpu().numpy(), 1024)
-    ws.append(isb.PackedWeight.from_codes(codes, 128, scales, s.int_scales, 1024))
+    alpha = int(os.environ.get("ISB_ALPHA", "1024"))
+    s = isb.integerize_scales(scales.cpu().numpy(), alpha)
+    ws.append(isb.PackedWeight.from_codes(codes, 128, scales, s.int_scales, alpha))
 q, sa = isb.quantize_per_token(torch.randn((m, k), device=dev))
 gemm = isb.gemm_integer_scale if path == "int" else isb.gemm_float_scale
 out = torch.empty((m, n), dtype=torch.bfloat16, device=dev)
