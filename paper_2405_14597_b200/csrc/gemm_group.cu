@@ -737,19 +737,25 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
       // writes: the 32 outputs' conversion chains (I2F.F64, 2 DMUL, F2F, F2F) are
       // independent and overlap; interleaving them with volatile smem accesses
       // serialised every chain (~260 cycles per output).
-      double sav[MT];  // integer path: s_a * 2^-e (exact), one DMUL per output left
+      // Integer path at MT = 32: two 16-token chunks. All MT factors and results live
+      // at once spilled (acc 64 + factors 64 + results 64 registers): M = 32 / 64 layer
+      // 39.0 / 68.4 -> 37.0 / 62.9 us. The float path measured ~1 % faster unchunked.
+      constexpr int kTC = MT > 16 && PATH == ISB_PATH_INTEGER_SCALE ? 16 : MT;
 #pragma unroll
-      for (int t = 0; t < MT; ++t)
-        sav[t] = PATH == ISB_PATH_INTEGER_SCALE ? sa_t[t] * q.inv_amp : sa_t[t];
-      uint32_t res[2][MT];
+      for (int t0 = 0; t0 < MT; t0 += kTC) {
+      double sav[kTC];  // integer path: s_a * 2^-e (exact), one DMUL per output left
+#pragma unroll
+      for (int t = 0; t < kTC; ++t)
+        sav[t] = PATH == ISB_PATH_INTEGER_SCALE ? sa_t[t0 + t] * q.inv_amp : sa_t[t0 + t];
+      uint32_t res[2][kTC];
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int t = 0; t < MT; ++t) {
-          const int32_t is = static_cast<int32_t>(acc[h][t]);
-          const float fs = __uint_as_float(acc[h][t]);
+        for (int t = 0; t < kTC; ++t) {
+          const int32_t is = static_cast<int32_t>(acc[h][t0 + t]);
+          const float fs = __uint_as_float(acc[h][t0 + t]);
           if ((PATH == ISB_PATH_INTEGER_SCALE && q.out_dtype == ISB_I32) || (p.dbg & 4096)) {
-            res[h][t] = acc[h][t];
+            res[h][t] = acc[h][t0 + t];
           } else {
             const float f = finish_eq<PATH>(is, fs, sav[t]);
             res[h][t] = ob == 4 ? __float_as_uint(f)
@@ -761,8 +767,8 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int t = 0; t < MT; ++t) {
-            const uint32_t dst = pb + t * (kTileN * 4) + (u + h * 64) * ob;
+          for (int t = 0; t < kTC; ++t) {
+            const uint32_t dst = pb + (t0 + t) * (kTileN * 4) + (u + h * 64) * ob;
             if (ob == 4)
               asm volatile("st.shared.u32 [%0], %1;" ::"r"(dst), "r"(res[h][t]) : "memory");
             else
@@ -774,8 +780,8 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int t = 0; t < MT; ++t) {
-            const int64_t m = static_cast<int64_t>(mt) * MT + t;
+          for (int t = 0; t < kTC; ++t) {
+            const int64_t m = static_cast<int64_t>(mt) * MT + t0 + t;
             const int64_t n = n0 + u + h * 64;
             if (n < n0 + nvalid && m < q.M) {
               if (ob == 4)
@@ -785,6 +791,7 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
                     static_cast<unsigned short>(res[h][t]);
             }
           }
+      }
       }
       if (bulk) {
         // 16-byte vector stores of the staged rows, consecutive threads along a row

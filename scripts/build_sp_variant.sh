@@ -2,6 +2,8 @@
 # Build a copy of libintscale_b200.so with a different prefill-kernel ring configuration
 # (gemm_sp.cu ISB_SP_NW / ISB_SP_NB) for A/B runs: ISB_LIB_PATH=<out> python ...
 # usage: scripts/build_sp_variant.sh NW NB out.so [extra nvcc flags, e.g. -DISB_SP_TRACE=1]
+# The isb_debug_set_flags measurement knobs of gemm_sp are compiled in only with
+# -DISB_SP_KNOBS=1 (the product build ignores them).
 set -e
 cd "$(dirname "$0")/../paper_2405_14597_b200/csrc"
 make -s all
