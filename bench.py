@@ -510,9 +510,10 @@ def run_ours(args, ws, rank, local):
     # Dominant kernel: the grouped layer launch (the whole step is this one kernel).
     achieved = layer_bytes / us_step / 1e3  # GB/s
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r02b_traffic.json")
-    if not os.path.exists(tpath):
-        tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    # the latest committed ncu capture of this kernel (dram read + write per launch)
+    tpath = next((os.path.join(ROOT, "profiles", f"{t}_traffic.json")
+                  for t in ("r02d", "r02b", "r02")
+                  if os.path.exists(os.path.join(ROOT, "profiles", f"{t}_traffic.json"))), "")
     if os.path.exists(tpath) and m == 16:
         try:
             with open(tpath) as f:

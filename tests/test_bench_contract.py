@@ -10,7 +10,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 import pytest
 
 
-@pytest.mark.parametrize("name", ["r01_bench_default.json", "r02b_bench_default.json"])
+@pytest.mark.parametrize("name", ["r01_bench_default.json", "r02b_bench_default.json",
+                                  "r02d_bench_default.json"])
 def test_bench_line_has_contract_keys(name):
     with open(os.path.join(ROOT, "profiles", name)) as f:
         d = json.load(f)
@@ -39,9 +40,9 @@ def test_bench_line_has_contract_keys(name):
 def test_latest_bench_line_roofline_evidence():
     """Every frac in the latest bench line recomputes from its own numbers, and the
     decode roofline's traffic equals dram read + write of the committed ncu capture of
-    the same kernel (profiles/r02b_group_int_m16_metrics.csv)."""
+    the same kernel (profiles/r02d_group_int_m16_metrics.csv or an earlier capture)."""
     import csv
-    with open(os.path.join(ROOT, "profiles", "r02b_bench_default.json")) as f:
+    with open(os.path.join(ROOT, "profiles", "r02d_bench_default.json")) as f:
         d = json.load(f)
     r = d["roofline"]
     assert abs(r["achieved"] - r["alg_bytes_per_launch"] / r["us_per_launch"] / 1e3) / r["achieved"] < 2e-3
@@ -49,7 +50,7 @@ def test_latest_bench_line_roofline_evidence():
     assert t["bound"] == "tensor" and abs(t["frac"] - t["achieved"] / t["peak"]) < 1e-3
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     totals = []
-    for tag in ("r02", "r02b"):  # the capture bench.py read its traffic figure from
+    for tag in ("r02", "r02b", "r02d"):  # the capture bench.py read its traffic figure from
         vals = {}
         with open(os.path.join(ROOT, "profiles", f"{tag}_group_int_m16_metrics.csv")) as f:
             for row in csv.DictReader(f):
