@@ -46,7 +46,7 @@ constexpr int kPgNP = 4;                        // TMEM partial slots (128 colum
 constexpr int kPgEW = 4;                        // epilogue warpgroups (MT / kPgEW tokens each)
 constexpr int kPgThreads = 128 + 128 + 128 * kPgEW;
 constexpr int kPgSmem = 1024 + kPgNA * kPgABytes + kPgSX * kPgXBytes + kPgSW * kBlockBytes +
-                        kPgNP * kTileN * 4 + 2 * kPgMT * 8 + 1024;
+                        kPgNP * kTileN * 4 + 4 * kPgMT * 8 + 1024;
 static_assert(kPgSmem <= 227 * 1024, "smem");
 static_assert(kPgNP * kPgMT <= 512, "TMEM");
 
@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(kPgThreads, 1)
   uint8_t* smem_w = smem_x + kPgSX * kPgXBytes;            // [SW][8 KiB] packed int4
   uint8_t* smem_sc = smem_w + kPgSW * kBlockBytes;         // [NP][128] group scales
   double* sa_s = reinterpret_cast<double*>(smem_sc + kPgNP * kTileN * 4);  // [2][MT]
-  uint64_t* wfull = reinterpret_cast<uint64_t*>(sa_s + 2 * kPgMT);
+  double* c52_s = sa_s + 2 * kPgMT;  // [2][MT] integer path: -2^52 * s_a * 2^-e per token
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(c52_s + 2 * kPgMT);
   uint64_t* wempty = wfull + kPgSW;
   uint64_t* xfull = wempty + kPgSW;
   uint64_t* xempty = xfull + kPgSX;
@@ -310,9 +311,20 @@ __global__ void __launch_bounds__(kPgThreads, 1)
       }
       cp_async_wait<1>();
       // integer path: s_a * 2^-e once per token (exact), not once per output
-      if (PATH == ISB_PATH_INTEGER_SCALE && te < kPgMT) sa_s[(it & 1) * kPgMT + te] *= p.inv_amp;
+      // and the DFMA's addend -2^52 * sa2, also once per token (exponent arithmetic on
+      // the ALU; a DMUL only for zero / subnormal / huge sa2) instead of per output
+      if (PATH == ISB_PATH_INTEGER_SCALE && te < kPgMT) {
+        const double sa2 = sa_s[(it & 1) * kPgMT + te] * p.inv_amp;
+        sa_s[(it & 1) * kPgMT + te] = sa2;
+        const int sh = __double2hiint(sa2);
+        c52_s[(it & 1) * kPgMT + te] =
+            (sh & 0x7FF00000) != 0 && (sh & 0x7FF00000) < 0x7C000000
+                ? __hiloint2double((sh + (52 << 20)) ^ static_cast<int>(0x80000000u), __double2loint(sa2))
+                : -sa2 * 4503599627370496.0;
+      }
       named_bar_sync(1, 128 * kPgEW);  // sa_s[it & 1] landed (and scaled) for every thread
       const double* sa_t = sa_s + (it & 1) * kPgMT + g * kCols;
+      const double* c52_t = c52_s + (it & 1) * kPgMT + g * kCols;
       const int64_t n = static_cast<int64_t>(nt) * kTileN + r;
       const int64_t m0 = static_cast<int64_t>(mt) * kPgMT + g * kCols;
       if (n < p.N) {
@@ -328,16 +340,10 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                 // Eq. 2 in one FP64 op (the FP64 pipe is the epilogue's scarce resource
                 // while the tensor core streams): D = 2^52 + |acc| by bit construction,
                 // fma(D, sa2, -2^52 sa2) = RN64(|acc| * sa2) exactly, sign after F2F
-                const double sa2 = sa_t[t];
                 const uint32_t a = static_cast<uint32_t>(iacc[t]);
                 const uint32_t mag = (a >> 31) ? 0u - a : a;
-                // -2^52 * sa2 by exponent arithmetic (ALU), DMUL only for zero / subnormal sa2
-                const int sh = __double2hiint(sa2);
-                const double c52 = (sh & 0x7FF00000) != 0 && (sh & 0x7FF00000) < 0x7C000000
-                                       ? __hiloint2double((sh + (52 << 20)) ^ static_cast<int>(0x80000000u),
-                                                          __double2loint(sa2))
-                                       : -sa2 * 4503599627370496.0;
-                const double o = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(mag)), sa2, c52);
+                const double o =
+                    __fma_rn(__hiloint2double(0x43300000, static_cast<int>(mag)), sa_t[t], c52_t[t]);
                 pg_store(p.out, p.out_dtype, idx,
                          __uint_as_float(__float_as_uint(__double2float_rn(o)) ^ (a & 0x80000000u)));
               }
