@@ -133,10 +133,11 @@ def test_prefill_pair_kernel_equals_one_cta_kernel():
             assert torch.equal(a, b), f"pair != 1-CTA at {(m, k, n)} {dt}"
 
 
-@pytest.mark.parametrize("m,k,n", [(2048, 512, 4096), (1024, 1024, 2560)])
+@pytest.mark.parametrize("m,k,n", [(2048, 512, 4096), (1024, 1024, 2560), (1000, 1152, 1000)])
 def test_prefill_general_alpha_8192_more_tiles_than_sms(m, k, n):
     """alpha = 8192 (k_g up to ~124, outside the fold band): the general per-group
-    epilogue at prefill M, many tiles, repeated."""
+    epilogue at prefill M, many tiles, repeated; K = 1152 has an odd group count and M, N
+    are ragged."""
     x, w, _, _, _ = llama_problem(m, k, n, seed_w=500 + n, seed_x=600 + m)
     s = O.integerize_scales(w.scales, 8192)
     assert s.int_scales.max() > 16
