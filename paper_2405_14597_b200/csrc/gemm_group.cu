@@ -666,13 +666,20 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
         if (lane == 0) mbar_arrive(&red_empty[buf]);
         continue;
       }
-      // the tile's accumulators for rows u and u + 64, all MT tokens
-      uint32_t acc[2][MT];
-      if (e.w < 0 || (p.dbg & 2048)) {
+      // the tile's accumulators for rows u and u + 64, all MT tokens (MT = 64: loaded
+      // per token chunk below — 2 x 64 accumulators do not fit next to the results)
+      constexpr bool kCL = MT > 32;
+      uint32_t acc[2][kCL ? 1 : MT];
+      const bool whole = e.w < 0 || (p.dbg & 2048);
+      const uint32_t* slots_f = nullptr;  // kCL: the finisher's slots, summed per chunk
+      int npieces_f = 0;
+      if (whole) {
+        if constexpr (!kCL) {
 #pragma unroll
-        for (int t = 0; t < MT; ++t) {
-          acc[0][t] = ld_shared_u32(pb + (t * kTileN + u) * 4);
-          acc[1][t] = ld_shared_u32(pb + (t * kTileN + u + 64) * 4);
+          for (int t = 0; t < MT; ++t) {
+            acc[0][t] = ld_shared_u32(pb + (t * kTileN + u) * 4);
+            acc[1][t] = ld_shared_u32(pb + (t * kTileN + u + 64) * 4);
+          }
         }
       } else {
         // a piece of a split tile: partial to the piece's slot; the piece that
@@ -700,7 +707,10 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
           if (lane == 0) mbar_arrive(&red_empty[buf]);
           continue;
         }
+        slots_f = slots;
+        npieces_f = npieces;
         // every slot's loads in flight together: one L2 round trip per piece
+        if constexpr (!kCL) {
 #pragma unroll
         for (int t = 0; t < MT; ++t) acc[0][t] = acc[1][t] = 0u;
         for (int k = 0; k < npieces; ++k) {
@@ -722,13 +732,14 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
                 acc[h][t] = __float_as_uint(__uint_as_float(acc[h][t]) + __uint_as_float(v[h][t]));
             }
         }
+        }
       }
       // Eq. 2 / Eq. 1 in place: the outputs overwrite the partial buffer ([t][128]
       // rows of out_dtype), then leave as 16-byte vector stores along the token
       // rows — 8x fewer store instructions than one 2-byte store per output, which
       // stall for microseconds in a memory system saturated by the weight stream
       // (a bulk-copy store would queue behind the SM's pending weight loads).
-      named_bar_sync(2, 64);  // every source word read before any is overwritten
+      if constexpr (!kCL) named_bar_sync(2, 64);  // every source word read before any is overwritten
       const int ob = q.out_dtype == ISB_F32 || q.out_dtype == ISB_I32 ? 4 : 2;
       const int64_t n0 = static_cast<int64_t>(nt) * kTileN;
       const int nvalid = static_cast<int>(min(static_cast<int64_t>(kTileN), q.N - n0));
@@ -740,9 +751,50 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
       // Integer path at MT = 32: two 16-token chunks. All MT factors and results live
       // at once spilled (acc 64 + factors 64 + results 64 registers): M = 32 / 64 layer
       // 39.0 / 68.4 -> 37.0 / 62.9 us. The float path measured ~1 % faster unchunked.
-      constexpr int kTC = MT > 16 && PATH == ISB_PATH_INTEGER_SCALE ? 16 : MT;
+      constexpr int kTC = (MT > 16 && PATH == ISB_PATH_INTEGER_SCALE) || kCL ? 16 : MT;
 #pragma unroll
       for (int t0 = 0; t0 < MT; t0 += kTC) {
+      uint32_t ac[2][kTC];  // this chunk's accumulators
+      if constexpr (kCL) {
+        if (whole) {
+#pragma unroll
+          for (int t = 0; t < kTC; ++t) {
+            ac[0][t] = ld_shared_u32(pb + ((t0 + t) * kTileN + u) * 4);
+            ac[1][t] = ld_shared_u32(pb + ((t0 + t) * kTileN + u + 64) * 4);
+          }
+          // the chunk's source words (its token rows, read by both warps) before any is
+          // overwritten; later chunks' rows are untouched by this chunk's outputs
+          named_bar_sync(2, 64);
+        } else {
+#pragma unroll
+          for (int t = 0; t < kTC; ++t) ac[0][t] = ac[1][t] = 0u;
+          for (int k = 0; k < npieces_f; ++k) {
+            const uint32_t* sl = slots_f + static_cast<int64_t>(k) * (MT * kTileN) + t0 * kTileN;
+            uint32_t v[2][kTC];
+#pragma unroll
+            for (int t = 0; t < kTC; ++t) {
+              v[0][t] = __ldcg(sl + t * kTileN + u);
+              v[1][t] = __ldcg(sl + t * kTileN + u + 64);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int t = 0; t < kTC; ++t) {
+                if (PATH == ISB_PATH_INTEGER_SCALE)
+                  ac[h][t] = static_cast<uint32_t>(static_cast<int32_t>(ac[h][t]) +
+                                                   static_cast<int32_t>(v[h][t]));
+                else
+                  ac[h][t] = __float_as_uint(__uint_as_float(ac[h][t]) + __uint_as_float(v[h][t]));
+              }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < kTC; ++t) {
+          ac[0][t] = acc[0][(t0 + t) % (kCL ? 1 : MT)];
+          ac[1][t] = acc[1][(t0 + t) % (kCL ? 1 : MT)];
+        }
+      }
       double sav[kTC];  // integer path: s_a * 2^-e (exact), one DMUL per output left
 #pragma unroll
       for (int t = 0; t < kTC; ++t)
@@ -752,10 +804,10 @@ __global__ void __launch_bounds__(Cfg<MT, false>::kThreads, 1)
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int t = 0; t < kTC; ++t) {
-          const int32_t is = static_cast<int32_t>(acc[h][t0 + t]);
-          const float fs = __uint_as_float(acc[h][t0 + t]);
+          const int32_t is = static_cast<int32_t>(ac[h][t]);
+          const float fs = __uint_as_float(ac[h][t]);
           if ((PATH == ISB_PATH_INTEGER_SCALE && q.out_dtype == ISB_I32) || (p.dbg & 4096)) {
-            res[h][t] = acc[h][t0 + t];
+            res[h][t] = ac[h][t];
           } else {
             const float f = finish_eq<PATH>(is, fs, sav[t]);
             res[h][t] = ob == 4 ? __float_as_uint(f)
@@ -884,17 +936,20 @@ int group_blocks_per_sm() {
 
 int group_capacity(int mt, int path, int num_sms) {
   static std::mutex mu;
-  static int cache[2][2] = {};
+  static int cache[3][2] = {};
   std::lock_guard<std::mutex> lk(mu);
-  int& slot = cache[mt == 16 ? 0 : 1][path == ISB_PATH_INTEGER_SCALE ? 1 : 0];
+  int& slot = cache[mt == 16 ? 0 : mt == 32 ? 1 : 2][path == ISB_PATH_INTEGER_SCALE ? 1 : 0];
   if (!slot) {
     int n = 0;
     if (mt == 16)
       n = path == ISB_PATH_INTEGER_SCALE ? group_blocks_per_sm<16, ISB_PATH_INTEGER_SCALE>()
                                          : group_blocks_per_sm<16, ISB_PATH_FLOAT_SCALE>();
-    else
+    else if (mt == 32)
       n = path == ISB_PATH_INTEGER_SCALE ? group_blocks_per_sm<32, ISB_PATH_INTEGER_SCALE>()
                                          : group_blocks_per_sm<32, ISB_PATH_FLOAT_SCALE>();
+    else
+      n = path == ISB_PATH_INTEGER_SCALE ? group_blocks_per_sm<64, ISB_PATH_INTEGER_SCALE>()
+                                         : group_blocks_per_sm<64, ISB_PATH_FLOAT_SCALE>();
     slot = n > 0 ? n : -1;
   }
   return slot > 0 ? slot * num_sms : 0;
@@ -956,7 +1011,15 @@ namespace {
 constexpr int64_t kGroupMaxM = 64;  // decode grouped kernel beyond this: prefill routes
 
 int pick_group_mt(int64_t max_m) {
-  return max_m <= 16 ? 16 : 32;  // 33..64 (and beyond) as 32-token tiles (gemm_tc.cu pick_mt)
+  // ISB_GROUP_MT=32 / 64 (A/B): the tile for 33 <= M <= 64 (default 64: one weight
+  // expansion per 64 tokens instead of one per 32)
+  static const int mt_big = [] {
+    const char* e = std::getenv("ISB_GROUP_MT");
+    return e && std::atoi(e) == 32 ? 32 : 64;
+  }();
+  if (max_m <= 16) return 16;
+  if (max_m <= 32) return 32;
+  return max_m <= 64 ? mt_big : 32;  // beyond 64: 32-token tiles (prefill M routes elsewhere)
 }
 
 // McNaughton wrap-around over `ncta` equal budgets. Tiles (cost = their 128-K
@@ -1083,7 +1146,7 @@ GroupPlan* group_plan_create(const isb_group_problem* probs, int nprob, int path
     }
     pl->mt = pick_group_mt(max_m);
     const int mt = pl->mt;
-    const int S = 4;  // Cfg<16/32>::S
+    const int S = mt == 64 ? Cfg<64, false>::S : Cfg<32, false>::S;
     if (own_bytes) cuda_check(cudaMalloc(&pl->owned, own_bytes), "cudaMalloc(group workspace)");
     uint8_t* own = static_cast<uint8_t*>(pl->owned);
     GParams& P = pl->prm;
@@ -1262,11 +1325,16 @@ void group_plan_run(GroupPlan* pl, cudaStream_t s) {
       launch_group_mt<16, ISB_PATH_INTEGER_SCALE>(pl->maps, pl->prm, pl->grid, s);
     else
       launch_group_mt<16, ISB_PATH_FLOAT_SCALE>(pl->maps, pl->prm, pl->grid, s);
-  } else {
+  } else if (pl->mt == 32) {
     if (pl->path == ISB_PATH_INTEGER_SCALE)
       launch_group_mt<32, ISB_PATH_INTEGER_SCALE>(pl->maps, pl->prm, pl->grid, s);
     else
       launch_group_mt<32, ISB_PATH_FLOAT_SCALE>(pl->maps, pl->prm, pl->grid, s);
+  } else {
+    if (pl->path == ISB_PATH_INTEGER_SCALE)
+      launch_group_mt<64, ISB_PATH_INTEGER_SCALE>(pl->maps, pl->prm, pl->grid, s);
+    else
+      launch_group_mt<64, ISB_PATH_FLOAT_SCALE>(pl->maps, pl->prm, pl->grid, s);
   }
 }
 

@@ -61,7 +61,7 @@ def single_reference(x, w, path, out_dtype):
     return q, sa, f(q, sa, w, out_dtype=out_dtype)
 
 
-@pytest.mark.parametrize("m", [1, 3, 16, 17, 32, 64])
+@pytest.mark.parametrize("m", [1, 3, 16, 17, 32, 40, 64])
 def test_group_layer_matches_k1_plus_k3(m):
     ws = layer_weights(LLAMA2_7B)
     gen = torch.Generator(device=DEV)
