@@ -43,7 +43,7 @@ struct Cfg {
   // Tile partials handed from the epilogue to the reduction warps (2/3), which do
   // the cluster split-K exchange + finalise off the epilogue's critical path.
   // MT = 128 (prefill) finalises straight from the epilogue's registers.
-  static constexpr int kPbufs = MT <= 32 ? 2 : (MT == 64 ? 1 : 0);
+  static constexpr int kPbufs = MT <= 64 ? 2 : 0;
   static constexpr int kPbufBytes = kPbufs * MT * kTileN * 4;
   static constexpr int kSaBytes = 2 * MT * 8;  // token scales, prefetched a tile ahead
   static constexpr int kFixed = 1024 + kXRes + kPbufBytes + kSaBytes + kAmaxBytes + 1024;

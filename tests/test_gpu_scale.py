@@ -250,7 +250,7 @@ from oracle import oracle as O
 from tests.instances import llama_problem
 import paper_2405_14597_b200 as isb
 dev = torch.device("cuda:0")
-for (m, k, n) in [(16, 4096, 4096), (32, 11008, 4096), (8, 4096, 22016)]:
+for (m, k, n) in {shapes}:
     x, w, s, _, _ = llama_problem(m, k, n, seed_w=77 + n, seed_x=78 + m)
     ref = O.gemm_integer_scale(x, w, s, workers=8)
     pw = isb.PackedWeight.from_codes(torch.from_numpy(w.values).to(dev), 128,
@@ -276,8 +276,20 @@ def test_decode_split_k_dsmem_stress(c):
     1000 back-to-back launches per shape at a forced split width (ISB_FORCE_C is
     read once per process, hence the subprocess)."""
     env = dict(os.environ, ISB_FORCE_C=c)
-    r = subprocess.run([sys.executable, "-c", _STRESS.format(root=ROOT, reps=1000)], cwd=ROOT,
-                       env=env, capture_output=True, text=True, timeout=900)
+    shapes = [(16, 4096, 4096), (32, 11008, 4096), (8, 4096, 22016)]
+    r = subprocess.run([sys.executable, "-c", _STRESS.format(root=ROOT, reps=1000, shapes=shapes)],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "stress ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+def test_decode_single_gemm_64_token_tiles():
+    """The opt-in 64-token single-GEMM decode tile (ISB_MT64=1, read once per process):
+    bit-exact against the oracle at 33 <= M <= 64 over repeated launches (its two
+    partial buffers alternate)."""
+    env = dict(os.environ, ISB_MT64="1")
+    shapes = [(64, 4096, 4096), (48, 11008, 4096), (64, 4096, 22016)]
+    r = subprocess.run([sys.executable, "-c", _STRESS.format(root=ROOT, reps=50, shapes=shapes)],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "stress ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
 
 
