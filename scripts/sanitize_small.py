@@ -1,4 +1,5 @@
-"""Small invocations of every kernel family for compute-sanitizer runs."""
+"""Small invocations of every kernel family for compute-sanitizer runs
+(scripts/sanitize.sh runs memcheck, synccheck and racecheck over it)."""
 import os
 import sys
 
@@ -30,9 +31,18 @@ for k, n in [(512, 384), (1024, 256)]:
     c, sc = isb.quantize_weight(llama_like_weight(k, n, gen, dev), 128, 4)
     si = isb.integerize_scales(sc.cpu().numpy(), 1024)
     ws.append(isb.PackedWeight.from_codes(c, 128, sc, si.int_scales, 1024))
-for mm in (16, 520):
+for mm in (16, 32, 48, 520):  # MT = 16 / 32 / 64 decode tiles, pair-kernel prefill
     g = isb.GroupedGemm([{"weight": w, "x": torch.randn((mm, w.k), device=dev)} for w in ws])
     g.run()
+# per-group prefill kernel on the general integer path (alpha = 8192, k_g > 16)
+x, w, _, xf, _ = llama_problem(600, 512, 384)
+s8192 = O.integerize_scales(w.scales, 8192)
+pw = isb.PackedWeight.from_codes(torch.from_numpy(w.values).to(dev), 128,
+                                 torch.from_numpy(w.scales).to(dev),
+                                 torch.from_numpy(s8192.int_scales).to(dev), s8192.amplifier)
+xq, sa = isb.quantize_per_token(torch.from_numpy(xf).to(dev))
+out = isb.gemm_integer_scale(xq, sa, pw, out_dtype=torch.float32)
+assert np.array_equal(out.cpu().numpy().view(np.int32), O.gemm_integer_scale(x, w, s8192).output.view(np.int32))
 xh = torch.randn((64, 512), device=dev).half()
 wh = (torch.randn((384, 512), device=dev) * 0.02).half()
 isb.gemm_dense(xh, wh)

@@ -50,7 +50,7 @@ def test_latest_bench_line_roofline_evidence():
     assert t["bound"] == "tensor" and abs(t["frac"] - t["achieved"] / t["peak"]) < 1e-3
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     totals = []
-    for tag in ("r02", "r02b", "r02d0", "r02d"):  # the capture bench.py read its traffic figure from
+    for tag in ("r02", "r02b", "r02d0", "r02d1", "r02d"):  # the capture bench.py read its traffic figure from
         vals = {}
         with open(os.path.join(ROOT, "profiles", f"{tag}_group_int_m16_metrics.csv")) as f:
             for row in csv.DictReader(f):
