@@ -1,7 +1,10 @@
 #!/bin/bash
 # compute-sanitizer memcheck / synccheck / racecheck over scripts/sanitize_small.py
 mkdir -p gpurun_out
+CS=${CS:-/usr/local/cuda/bin/compute-sanitizer}
 for tool in memcheck synccheck racecheck; do
   echo "== $tool"
-  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_small.py 2>&1 | grep -E "COMPUTE-SANITIZER|ERROR SUMMARY|sanitize run ok|Error|Race|hazard" | head -40
+  timeout 1200 $CS --tool $tool --print-limit 20 python scripts/sanitize_small.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "rc=$?"
+  grep -E "ERROR SUMMARY|RACECHECK SUMMARY|sanitize run ok|Traceback|Error:" gpurun_out/sanitize_$tool.log | head -20
 done
