@@ -69,7 +69,7 @@ if __name__ == "__main__":
     tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
     names = (["group_int_m16", "group_float_m16", "pf_sp_gu_m2048", "pf_group_m2048",
               "pf_float_gu_m2048"] if tag == "r02b" else
-             ["group_int_m16", "group_float_m16", "group_int_m32", "group_float_m32",
+             ["group_int_m16", "group_float_m16", "group_int_m32", "group_float_m32", "group_int_m64",
               "pf_sp_gu_m2048", "pf_group_m2048", "pf_float_gu_m2048", "pf_int8192_gu_m2048"]
              if tag == "r02d" else
              ["group_int_m16", "group_float_m16", "group_int_m1", "pf_int_m2048", "pf_float_m2048"])
