@@ -9,18 +9,19 @@
 // the Atom-style fp32 form: acc += float(P_g) * float(s_g), out = float(acc * s_a).
 //
 // Tile: 128 output channels x 128 tokens. Per 128-K block (one group, g = 128) the
-// tensor core writes the group's int32 partial 16*P_g into one of kNP TMEM slots;
-// four epilogue warpgroups (32 tokens each, one TMEM lane = one channel per thread)
-// drain it and accumulate in registers
-//   integer:  acc += P16 * k_g   (one IMAD; >> 4 once at the end when 16x the
-//                                 static bound fits int32, else (P16 >> 4) * k_g)
-//   float:    acc  = fma(float(P16), s_g / 16, acc)   (I2F + FFMA)
+// tensor core writes the group's int32 partial into one of kNP TMEM slots; four
+// epilogue warpgroups (32 tokens each, one TMEM lane = one channel per thread) drain
+// it and accumulate in registers
+//   integer:  acc += P_g * k_g   (one IMAD; the transform expands the int4 codes
+//                                 themselves, so the partial is P_g)
+//   float:    acc  = fma(float(P16), s_g / 16, acc)   (I2F + FFMA; the transform
+//                                 expands 16*code, two ops per word, P16 = 16 P_g)
 // while the MMA fills the next slots. Roles:
 //   warp 0        packed int4 weights -> W ring (bulk copies)
 //   warp 1        MMA issuer (tcgen05.mma.cta_group::1.kind::i8, SS)
 //   warp 2        TMEM owner + group scales -> scale ring (one slot per partial)
 //   warp 3        int8 activation tiles -> X ring (TMA, SWIZZLE_128B)
-//   warps 4-7     transform: int4 -> 16*code int8 into the SW128 A ring
+//   warps 4-7     transform: int4 -> int8 (code / 16*code) into the SW128 A ring
 //   warps 8-23    epilogue
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -224,8 +225,17 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         const uint32_t w4[4] = {q[c].x, q[c].y, q[c].z, q[c].w};
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-          a[c * 8 + 2 * w] = (w4[w] << 4) & 0xF0F0F0F0u;  // 16*code(k0..k0+3)
-          a[c * 8 + 2 * w + 1] = w4[w] & 0xF0F0F0F0u;     // 16*code(k0+4..k0+7)
+          if constexpr (PATH == ISB_PATH_INTEGER_SCALE) {
+            // code itself (sign-extended nibble per byte: ((n ^ 8) + 0x78) ^ 0x80, no
+            // carry leaves a byte), so the epilogue's partial is P_g and acc += P_g * k_g
+            // is one IMAD per value (no >> 4)
+            a[c * 8 + 2 * w] = (((w4[w] & 0x0F0F0F0Fu) ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
+            a[c * 8 + 2 * w + 1] =
+                ((((w4[w] >> 4) & 0x0F0F0F0Fu) ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
+          } else {
+            a[c * 8 + 2 * w] = (w4[w] << 4) & 0xF0F0F0F0u;  // 16*code(k0..k0+3)
+            a[c * 8 + 2 * w + 1] = w4[w] & 0xF0F0F0F0u;     // 16*code(k0+4..k0+7)
+          }
         }
       }
       mbar_wait(&a_empty[as], ((j / kPgNA) & 1) ^ 1);
@@ -247,7 +257,6 @@ __global__ void __launch_bounds__(kPgThreads, 1)
     const int te = static_cast<int>(ew * 32 + lane);
     const uint32_t r = q * 32 + lane;                 // TMEM lane == channel in tile
     const uint32_t lane_base = (q * 32) << 16;
-    const bool late = p.late_shift != 0;
     pdl_wait();
     auto sa_prefetch = [&](int it) {
       if (it < ntiles) {
@@ -290,9 +299,9 @@ __global__ void __launch_bounds__(kPgThreads, 1)
           tmem_wait_ld();
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
-            const int32_t d = static_cast<int32_t>(v[t]);  // 16 * P_g, exact
+            const int32_t d = static_cast<int32_t>(v[t]);  // P_g (integer) / 16 * P_g (float)
             if (PATH == ISB_PATH_INTEGER_SCALE)
-              iacc[cc + t] += late ? d * k : (d >> 4) * k;
+              iacc[cc + t] += d * k;
             else
               facc[cc + t] = fmaf(static_cast<float>(d), s16, facc[cc + t]);
           }
@@ -305,10 +314,6 @@ __global__ void __launch_bounds__(kPgThreads, 1)
         }
       }
       // tile done: Eq. 2 / Eq. 1 per output
-      if (PATH == ISB_PATH_INTEGER_SCALE && late) {
-#pragma unroll
-        for (int t = 0; t < kCols; ++t) iacc[t] >>= 4;  // exact: 16 | acc16
-      }
       cp_async_wait<1>();
       // integer path: s_a * 2^-e once per token (exact), not once per output
       // and the DFMA's addend -2^52 * sa2, also once per token (exponent arithmetic on
